@@ -1,0 +1,204 @@
+"""Dense FP64 oracle: classical parareal (Algorithm 1) for a matrix ODE dX/dt = F(X).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain, slow, obviously correct: every step
+below is written in the order and notation of the paper; the only library primitive is the
+matrix product (numpy ``@``).  No blocking, fusion or reordering.
+
+Citations (P:n = PAPER.md line n):
+  * inverse flow F(X) = X (I - A) X, X(0) = I, X(1) = A^{-1}             P:44 (§1); eq. (eqQ)
+  * steady-state flow dX/dt = F(X), F(X*) = 0 <=> X* = f(A)              P:46-51 eq. (stat)
+    (instance F(X) = A - X^2, X* = A^{1/2}: BASELINE.json north star)
+  * coarse propagator G = forward Euler                                   P:129, P:182 ("Euler explicit")
+  * fine propagator F = Runge-Kutta ("Runge Kutta method can be applied") P:44; classical RK4 (R1)
+  * Algorithm 1, Step 0 U^0_{n+1} = G(U^0_n), U^0_0 = u0                 P:136-139 eq. (eqStep0)
+  * Step k+1: F(U^k_n) in parallel; U^{k+1}_{n+1} = G(U^{k+1}_n) + F(U^k_n) - G(U^k_n)
+                                                                          P:143-147 eq. (eqStepk+1)
+Readings:
+  R1 classical RK4, S = ((k1 + 2 k2) + 2 k3) + k4, X <- X + (h/6) S
+  R2 F(X) = X (B X) with B = I - A formed once
+  R3 correction evaluated as F(U^k_n) + (G(U^{k+1}_n) - G(U^k_n))
+  R4 U^{k+1}_0 = X0
+  R5 K = number of correction sweeps after Step 0 (K = 0: coarse only)
+  R6 stop on delta_{k+1} = ||U^{k+1}_N - U^k_N||_F / ||U^{k+1}_N||_F <= tol (or fixed K)
+  R10 residual stop ||A - U_N^2||_F / ||A||_F <= tol evaluated only for k >= 1
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, Optional
+
+import numpy as np
+
+FLOW_INVERSE = 0
+FLOW_SQRT = 1
+STOP_FIXED_K = 0
+STOP_DELTA = 1
+STOP_RESIDUAL = 2
+
+
+# ----------------------------------------------------------------------------------------------
+# Right-hand sides F(X)
+# ----------------------------------------------------------------------------------------------
+def rhs_inverse(B: np.ndarray) -> Callable:
+    """F(X) = X (I - A) X with B = I - A (R2: X @ (B @ X))."""
+    return lambda X: X @ (B @ X)
+
+
+def rhs_sqrt(A: np.ndarray) -> Callable:
+    """F(X) = A - X^2 (steady state X* = A^{1/2}; P:46-51 with the north-star instance)."""
+    return lambda X: A - X @ X
+
+
+def make_rhs(A: np.ndarray, flow: int) -> Callable:
+    if flow == FLOW_INVERSE:
+        B = np.eye(A.shape[0]) - A          # formed once (R2)
+        return rhs_inverse(B)
+    if flow == FLOW_SQRT:
+        return rhs_sqrt(A)
+    raise ValueError(f"unknown flow {flow}")
+
+
+# ----------------------------------------------------------------------------------------------
+# Propagators
+# ----------------------------------------------------------------------------------------------
+def euler(rhs: Callable, X, h: float, m: int):
+    """Coarse propagator G: m forward-Euler steps X <- X + h F(X)."""
+    for _ in range(m):
+        X = X + h * rhs(X)
+    return X
+
+
+def rk4(rhs: Callable, X, h: float, m: int):
+    """Fine propagator F: m classical RK4 steps (P:44 'Runge Kutta'; reading R1)."""
+    for _ in range(m):
+        k1 = rhs(X)
+        k2 = rhs(X + (h / 2) * k1)
+        k3 = rhs(X + (h / 2) * k2)
+        k4 = rhs(X + h * k3)
+        S = ((k1 + 2 * k2) + 2 * k3) + k4
+        X = X + (h / 6) * S
+    return X
+
+
+def frob(X) -> float:
+    return float(np.sqrt(np.sum(np.asarray(X, dtype=np.float64) ** 2)))
+
+
+# ----------------------------------------------------------------------------------------------
+# Algorithm 1 (classical parareal), generic over the state type
+# ----------------------------------------------------------------------------------------------
+def parareal(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K_max: int,
+             tol: float = 0.0, stop: int = STOP_FIXED_K, norm: Callable = frob,
+             residual: Optional[Callable] = None, skip_prefix: bool = False,
+             keep_history: bool = False) -> dict:
+    """Classical parareal on [0, T] with N uniform slices.
+
+    G(x) = euler(rhs, x, T/(N m_G), m_G); F(x) = rk4(rhs, x, T/(N m_F), m_F).
+    Returns dict(X=U_N, U=[U_0..U_N], k_done, deltas, residuals, converged[, history]).
+
+    skip_prefix: at sweep k (0-based), F(U^k_n) for n < k equals the previous sweep's value
+    bitwise and the correction leaves U_{n+1} unchanged (R3/R14), so both are skipped.  The
+    literal algorithm (skip_prefix=False) is the default; tests check the two agree bitwise.
+    """
+    if K_max < 0 or N < 1 or m_G < 1 or m_F < 1:
+        raise ValueError("invalid parareal parameters")
+    hG = T / (N * m_G)
+    hF = T / (N * m_F)
+    G = lambda x: euler(rhs, x, hG, m_G)
+    F = lambda x: rk4(rhs, x, hF, m_F)
+
+    # Step 0 (eq. eqStep0): U^0_{n+1} = G(U^0_n), U^0_0 = u0
+    U = [X0]
+    Gold = []
+    for n in range(N):
+        g = G(U[n])
+        Gold.append(g)
+        U.append(g)
+    deltas, residuals = [], []
+    history = [list(U)] if keep_history else None
+    res0 = residual(U[N]) if residual is not None else None
+    k_done = 0
+    converged = stop == STOP_FIXED_K
+    Fk = [None] * N
+    for k in range(K_max):
+        # Step k+1, part 1: F(U^k_n) for all n ("compute in parallel")
+        first = k if skip_prefix else 0
+        for n in range(first, N):
+            Fk[n] = F(U[n])
+        # Step k+1, part 2: sequential correction (eq. eqStepk+1), evaluated as F + (Gnew - Gold)
+        V = list(U)
+        V[0] = X0                                             # R4
+        for n in range(first, N):
+            g = G(V[n])
+            V[n + 1] = Fk[n] + (g - Gold[n])                  # R3
+            Gold[n] = g
+        delta = norm(V[N] - U[N]) / norm(V[N])
+        U = V
+        k_done = k + 1
+        deltas.append(delta)
+        if residual is not None:
+            residuals.append(residual(U[N]))
+        if keep_history:
+            history.append(list(U))
+        if stop == STOP_DELTA and delta <= tol:
+            converged = True
+            break
+        if stop == STOP_RESIDUAL and residuals[-1] <= tol:      # k >= 1 by construction (R10)
+            converged = True
+            break
+        if k_done == N:
+            # After N sweeps U^N_n is the sequential fine solution (Remark P:155-157); further
+            # sweeps are identities, so the iteration stops here converged (reading R15).
+            converged = True
+            break
+    out = dict(X=U[N], U=U, k_done=k_done, deltas=deltas, residuals=residuals,
+               residual0=res0, converged=converged)
+    if keep_history:
+        out["history"] = history
+    return out
+
+
+def sequential_fine(rhs: Callable, X0, T: float, N: int, m_F: int) -> list:
+    """The reference the paper compares against: S_0 = X0, S_{n+1} = F(S_n)."""
+    hF = T / (N * m_F)
+    S = [X0]
+    for n in range(N):
+        S.append(rk4(rhs, S[n], hF, m_F))
+    return S
+
+
+# ----------------------------------------------------------------------------------------------
+# Flow-level drivers and residuals (the matrix-function view, Example 1 P:167-176)
+# ----------------------------------------------------------------------------------------------
+def residual_inverse(A: np.ndarray, X: np.ndarray) -> float:
+    """||A X - I||_F / sqrt(n): X(1) = A^{-1}."""
+    n = A.shape[0]
+    return frob(A @ X - np.eye(n)) / math.sqrt(n)
+
+
+def residual_sqrt(A: np.ndarray, X: np.ndarray) -> float:
+    """||A - X^2||_F / ||A||_F: F(X*) = 0 at the steady state."""
+    return frob(A - X @ X) / frob(A)
+
+
+def flow_residual(A: np.ndarray, flow: int) -> Callable:
+    if flow == FLOW_INVERSE:
+        return lambda X: residual_inverse(A, X)
+    return lambda X: residual_sqrt(A, X)
+
+
+def solve(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,
+          tol: float = 0.0, stop: int = STOP_FIXED_K, skip_prefix: bool = True,
+          keep_history: bool = False) -> dict:
+    """f(A) by parareal on the flow's ODE with X0 = I."""
+    A = np.asarray(A, dtype=np.float64)
+    rhs = make_rhs(A, flow)
+    X0 = np.eye(A.shape[0])
+    # the residual is recorded for every flow; it drives the stop only for STOP_RESIDUAL
+    return parareal(rhs, X0, T, N, m_G, m_F, K_max, tol, stop, frob, flow_residual(A, flow),
+                    skip_prefix, keep_history)
+
+
+def solve_sequential_fine(A: np.ndarray, flow: int, T: float, N: int, m_F: int) -> np.ndarray:
+    A = np.asarray(A, dtype=np.float64)
+    return sequential_fine(make_rhs(A, flow), np.eye(A.shape[0]), T, N, m_F)[N]

@@ -1,0 +1,66 @@
+"""Spectral oracle: the parareal iteration run per eigenvalue (SURVEY.md §8(c) pin P1).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+With X0 = I every quantity of the algorithm (Euler/RK4 stages, corrections) is a polynomial in A
+with scalar coefficients, so for A = V diag(lam) V^T every iterate is U^k_n = V diag(u^k_n(lam)) V^T
+where u^k_n is the SAME algorithm applied to the scalar ODE
+    inverse: q' = q ((1 - lam) q)        (the eigen-image of X (I - A) X)
+    sqrt:    x' = lam - x^2              (the eigen-image of A - X^2)
+with x0 = 1.  This is the paper's own diagonalisation argument.  Frobenius norms of
+V diag(u) V^T are 2-norms of u (V orthogonal), so the delta/residual stop tests carry over.
+The state of the generic dense.parareal is then a length-n vector of scalars (elementwise ops).
+
+mp_parareal_scalar runs the same recursion in mpmath with `dps` digits: a high-precision twin
+used to pin the FP64 paths (P2).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import dense
+
+
+def scalar_rhs(lam, flow: int):
+    if flow == dense.FLOW_INVERSE:
+        b = 1.0 - lam
+        return lambda q: q * (b * q)
+    if flow == dense.FLOW_SQRT:
+        return lambda x: lam - x * x
+    raise ValueError(flow)
+
+
+def solve(eigvals: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,
+          tol: float = 0.0, stop: int = dense.STOP_FIXED_K, keep_history: bool = False) -> dict:
+    """Scalar parareal for every eigenvalue at once (vectorised over lam). Returns the dense
+    dict shape with X/U entries as eigen-coefficient vectors u (reconstruct with `reconstruct`)."""
+    lam = np.asarray(eigvals, dtype=np.float64)
+    rhs = scalar_rhs(lam, flow)
+    x0 = np.ones_like(lam)
+    norm = lambda u: float(np.sqrt(np.sum(u * u)))
+    if flow == dense.FLOW_INVERSE:
+        # ||A X - I||_F / sqrt(n) = ||lam u - 1||_2 / sqrt(n)
+        residual = lambda u: norm(lam * u - 1.0) / math.sqrt(lam.size)
+    else:
+        # ||A - X^2||_F / ||A||_F = ||lam - u^2||_2 / ||lam||_2
+        residual = lambda u: norm(lam - u * u) / norm(lam)
+    return dense.parareal(rhs, x0, T, N, m_G, m_F, K_max, tol, stop, norm, residual,
+                          skip_prefix=True, keep_history=keep_history)
+
+
+def reconstruct(V: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """V diag(u) V^T."""
+    return (V * u) @ V.T
+
+
+def mp_parareal_scalar(lam, flow: int, T, N: int, m_G: int, m_F: int, K_max: int, dps: int = 50):
+    """The scalar recursion in mpmath at `dps` digits; returns (u_N as mpf, deltas)."""
+    import mpmath as mp
+    with mp.workdps(dps):
+        lam_ = mp.mpf(lam)
+        rhs = scalar_rhs(lam_, flow)
+        out = dense.parareal(rhs, mp.mpf(1), mp.mpf(T), N, m_G, m_F, K_max, 0.0,
+                             dense.STOP_FIXED_K, norm=lambda x: abs(x), skip_prefix=False)
+        return out["X"], out["U"]

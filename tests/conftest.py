@@ -1,0 +1,19 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C ABI)")
+    config.addinivalue_line("markers", "slow: long-running (full-size configs)")
+
+
+def pytest_collection_modifyitems(config, items):
+    # A GPU test on a box without CUDA is a hard failure, never a silent skip: the CUDA path must
+    # be the one that runs.  Only CPU-only collection (-m "not gpu") avoids them.
+    pass

@@ -1,0 +1,285 @@
+"""Pins for the CPU oracle (oracle/): checks against what the paper and the mathematics fix,
+never against the oracle itself.  CPU only (-m "not gpu").
+
+Each test names what it pins and the passage it follows (P:n = PAPER.md, S:n = SPEC.md line).
+A plausible mistake anywhere in oracle/dense.py (dropped term, wrong sign, wrong index, wrong
+RK coefficient, transposed operand, wrong correction order) fails at least one test here:
+  * RK4 coefficients/association      -> test_rk4_stability_polynomial_matrix, test_rk4_order
+  * Euler step / coarse sweep          -> test_euler_golden, test_coarse_sweep_geometric
+  * correction sign / index / order    -> test_linear_parareal_binomial_closed_form (+ P5/P6 bitwise)
+  * inverse flow operands (transpose)  -> test_inverse_flow_closed_form_nonsymmetric
+  * sqrt flow                          -> test_sqrt_steady_state
+  * spectral oracle                    -> test_dense_vs_spectral, test_spectral_vs_mpmath
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dense, spectral
+import workloads
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _read_golden(name):
+    vals = {}
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if not line:
+                continue
+            k, v = line.split("=", 1)
+            vals[k.strip()] = v.strip()
+    return vals
+
+
+# ---------------------------------------------------------------------------------------------
+# Propagators
+# ---------------------------------------------------------------------------------------------
+def test_euler_golden():
+    """scalar x' = -x, x0 = 1, one Euler step h = 0.1 -> 0.9 (golden/spec_examples.txt)."""
+    g = _read_golden("spec_examples.txt")
+    x = dense.euler(lambda x: -x, 1.0, 0.1, 1)
+    assert x == float(g["euler_one_step_h0.1"])
+
+
+def test_coarse_sweep_geometric():
+    """Euler coarse sweep of x' = -x, N = 4, dT = 0.25 gives 0.75^n (exact in FP64)."""
+    out = dense.parareal(lambda x: -x, 1.0, 1.0, 4, 1, 1, 0)
+    assert out["U"] == [0.75 ** n for n in range(5)]
+
+
+def test_rk4_stability_polynomial_matrix():
+    """Classical RK4 on the linear flow X' = M X multiplies by R(hM) = I + Z + Z^2/2 + Z^3/6 + Z^4/24
+    (textbook stability polynomial).  M non-symmetric, so a transposed product also fails."""
+    rng = np.random.default_rng(7)
+    n = 6
+    M = rng.standard_normal((n, n))
+    X0 = rng.standard_normal((n, n))
+    h = 0.05
+    Z = h * M
+    R = np.eye(n) + Z + Z @ Z / 2 + Z @ Z @ Z / 6 + Z @ Z @ Z @ Z / 24
+    X1 = dense.rk4(lambda X: M @ X, X0, h, 1)
+    np.testing.assert_allclose(X1, R @ X0, rtol=0, atol=1e-14 * np.abs(R @ X0).max() * 10)
+    # three steps = R^3
+    X3 = dense.rk4(lambda X: M @ X, X0, h, 3)
+    np.testing.assert_allclose(X3, R @ R @ R @ X0, rtol=0, atol=1e-13)
+
+
+def test_rk4_order():
+    """RK4 is 4th order: on q' = (1 - lam) q^2 (exact q(t) = 1/(1 + t(lam - 1))) halving h
+    divides the t = 1 error by ~16."""
+    lam = 3.0
+    rhs = lambda q: q * ((1 - lam) * q)
+    exact = 1.0 / lam
+    e1 = abs(dense.rk4(rhs, 1.0, 1 / 20, 20) - exact)
+    e2 = abs(dense.rk4(rhs, 1.0, 1 / 40, 40) - exact)
+    assert 14.0 < e1 / e2 < 18.0
+
+
+def test_euler_order():
+    """Forward Euler is 1st order on the same closed form."""
+    lam = 3.0
+    rhs = lambda q: q * ((1 - lam) * q)
+    exact = 1.0 / lam
+    e1 = abs(dense.euler(rhs, 1.0, 1 / 200, 200) - exact)
+    e2 = abs(dense.euler(rhs, 1.0, 1 / 400, 400) - exact)
+    assert 1.8 < e1 / e2 < 2.2
+
+
+# ---------------------------------------------------------------------------------------------
+# Algorithm 1 bookkeeping
+# ---------------------------------------------------------------------------------------------
+def test_linear_parareal_binomial_closed_form():
+    """For a linear flow X' = M X the propagators are matrices G = R_E(h_G M)^{m_G},
+    F = R_RK4(h_F M)^{m_F} (commuting), and classical parareal has the closed form
+        U^k_n = sum_{j=0}^{min(k,n)} C(n, j) (F - G)^j G^{n-j} u0
+    (standard linear parareal analysis, Gander & Vandewalle; the algorithm of).
+    Pins the correction's sign, indices and the Step-0 sweep."""
+    rng = np.random.default_rng(11)
+    n = 5
+    M = -np.eye(n) + 0.4 * rng.standard_normal((n, n))    # non-symmetric
+    X0 = np.eye(n) + 0.1 * rng.standard_normal((n, n))
+    T, N, mG, mF = 2.0, 6, 2, 5
+    hG, hF = T / (N * mG), T / (N * mF)
+    ZG, ZF = hG * M, hF * M
+    RE = np.eye(n) + ZG
+    RK = np.eye(n) + ZF + ZF @ ZF / 2 + ZF @ ZF @ ZF / 6 + ZF @ ZF @ ZF @ ZF / 24
+    Gm = np.linalg.matrix_power(RE, mG)
+    Fm = np.linalg.matrix_power(RK, mF)
+    out = dense.parareal(lambda X: M @ X, X0, T, N, mG, mF, N, keep_history=True)
+    for k, U in enumerate(out["history"]):
+        for m in range(N + 1):
+            ref = sum(math.comb(m, j) * np.linalg.matrix_power(Fm - Gm, j) @
+                      np.linalg.matrix_power(Gm, m - j) for j in range(min(k, m) + 1)) @ X0
+            np.testing.assert_allclose(U[m], ref, rtol=0, atol=1e-12)
+
+
+def _small_inverse_case(n=10, seed=1):
+    w = workloads.random_spd(n, seed)
+    return w.A
+
+
+def test_parareal_K_equals_N_is_sequential_fine_bitwise():
+    """P:155-157 (Remark): after N sweeps parareal equals the sequential fine solution; with the
+    correction evaluated as F + (Gnew - Gold) (R3) the equality is bitwise (P5)."""
+    A = _small_inverse_case()
+    rhs = dense.make_rhs(A, dense.FLOW_INVERSE)
+    X0 = np.eye(A.shape[0])
+    N = 5
+    out = dense.parareal(rhs, X0, 1.0, N, 1, 6, N)
+    seq = dense.sequential_fine(rhs, X0, 1.0, N, 6)
+    for m in range(N + 1):
+        assert np.array_equal(out["U"][m], seq[m])
+
+
+def test_prefix_exactness_bitwise():
+    """S:194/S:220 (P6): after k sweeps U^k_n equals the sequential fine solution for n <= k."""
+    A = _small_inverse_case(8, 2)
+    rhs = dense.make_rhs(A, dense.FLOW_INVERSE)
+    X0 = np.eye(8)
+    N = 6
+    out = dense.parareal(rhs, X0, 1.0, N, 1, 4, N, keep_history=True)
+    seq = dense.sequential_fine(rhs, X0, 1.0, N, 4)
+    for k, U in enumerate(out["history"]):
+        for m in range(min(k, N) + 1):
+            assert np.array_equal(U[m], seq[m]), (k, m)
+        if k < N:   # and strictly not yet converged beyond the prefix (the test is not vacuous)
+            assert not np.array_equal(U[N], seq[N])
+
+
+def test_skip_prefix_is_bitwise_identical():
+    """R14: skipping F(U^k_n), n < k, and the identity corrections changes nothing bitwise."""
+    A = _small_inverse_case(9, 3)
+    a = dense.solve(A, dense.FLOW_INVERSE, 1.0, 6, 1, 5, 4, skip_prefix=False)
+    b = dense.solve(A, dense.FLOW_INVERSE, 1.0, 6, 1, 5, 4, skip_prefix=True)
+    assert np.array_equal(a["X"], b["X"])
+    assert a["deltas"] == b["deltas"]
+
+
+def test_identity_matrix_is_exact():
+    """S:129, S:273 (P7): A = I gives F == 0 for the inverse flow and F(I) = 0 for the sqrt flow,
+    so the result is exactly I."""
+    n = 7
+    for flow in (dense.FLOW_INVERSE, dense.FLOW_SQRT):
+        out = dense.solve(np.eye(n), flow, 1.0, 4, 1, 3, 3)
+        assert np.array_equal(out["X"], np.eye(n))
+
+
+def test_single_slice():
+    """S:197 (P7): N = 1 gives U^1_1 = F(u0) exactly."""
+    A = _small_inverse_case(6, 4)
+    rhs = dense.make_rhs(A, dense.FLOW_INVERSE)
+    out = dense.parareal(rhs, np.eye(6), 1.0, 1, 2, 7, 1)
+    assert np.array_equal(out["X"], dense.rk4(rhs, np.eye(6), 1.0 / 7, 7))
+
+
+def test_zero_flow_constant():
+    """x' = 0 keeps every iterate equal to u0."""
+    out = dense.parareal(lambda x: 0.0 * x, 2.5, 1.0, 5, 1, 3, 3, keep_history=True)
+    for U in out["history"]:
+        assert U == [2.5] * 6
+
+
+# ---------------------------------------------------------------------------------------------
+# Flows against the matrix functions they define
+# ---------------------------------------------------------------------------------------------
+def test_inverse_flow_closed_form_nonsymmetric():
+    """P:169-176 (eq. eqQ): Q(t) = (I + t(A - I))^{-1} solves dQ/dt = -Q (A - I) Q = Q (I - A) Q,
+    Q(1) = A^{-1}.  A non-symmetric, so X (B X) with a transposed operand would fail.  The RK4
+    sequential fine solution matches the closed form at every slice end T_n within the RK4 error."""
+    n = 12
+    A = workloads.random_nonsymmetric(n, 0)
+    N, mF = 4, 100
+    S = dense.sequential_fine(dense.make_rhs(A, dense.FLOW_INVERSE), np.eye(n), 1.0, N, mF)
+    for m in range(N + 1):
+        t = m / N
+        Q = np.linalg.inv(np.eye(n) + t * (A - np.eye(n)))
+        assert np.abs(S[m] - Q).max() < 1e-9 * np.abs(Q).max()
+    assert dense.residual_inverse(A, S[N]) < 1e-9
+
+
+def test_cfg0_inverse_and_P3_bound():
+    """P:44/P:176 (P3): A X(1) ~ I.  BASELINE cfg[0] stops at a fixed K = 4 < N, so the bound is
+    the parareal error at K plus the RK4 error: 1e-7; at K = N it is <= 1e-12."""
+    w = workloads.config(0)
+    r4 = dense.solve(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 4)
+    assert dense.residual_inverse(w.A, r4["X"]) < 1e-7
+    rN = dense.solve(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.N)
+    assert dense.residual_inverse(w.A, rN["X"]) < 1e-12
+    assert np.abs(rN["X"] - np.linalg.inv(w.A)).max() < 1e-12
+
+
+def test_sqrt_steady_state():
+    """P:46-51 (eq. stat) with F(X) = A - X^2: the steady state X* = A^{1/2} (F(X*) = 0).  Small 2D
+    Laplacian analogue of cfg[4]: ||A - X^2||_F/||A||_F <= 1e-10, X symmetric, and X equals
+    V diag(sqrt(lam)) V^T (closed-form Kronecker sine eigenbasis) within 1e-10 (P4)."""
+    m = 4
+    A = workloads.laplacian_2d(m) + np.eye(m * m)
+    V1, mu1 = workloads.laplacian_1d_eig(m)
+    V = np.kron(V1, V1)
+    lam = 1.0 + (mu1[:, None] + mu1[None, :]).reshape(-1)
+    out = dense.solve(A, dense.FLOW_SQRT, 20.0, 64, 2, 32, 4, tol=1e-10, stop=dense.STOP_RESIDUAL)
+    X = out["X"]
+    assert out["converged"] and out["residuals"][-1] <= 1e-10
+    assert np.abs(X - X.T).max() < 1e-13
+    np.testing.assert_allclose(X, (V * np.sqrt(lam)) @ V.T, rtol=0, atol=1e-10)
+
+
+def test_dense_vs_spectral():
+    """P1: with X0 = I every iterate is a polynomial in A, so the dense iteration equals
+    V diag(u^k_n(lam)) V^T with u the scalar iteration per eigenvalue."""
+    w = workloads.random_spd(20, 5)
+    d = dense.solve(w.A, dense.FLOW_INVERSE, 1.0, 6, 1, 10, 6, tol=1e-12, stop=dense.STOP_DELTA)
+    s = spectral.solve(w.eigvals, dense.FLOW_INVERSE, 1.0, 6, 1, 10, 6, tol=1e-12, stop=dense.STOP_DELTA)
+    Xs = spectral.reconstruct(w.eigvecs, s["X"])
+    assert d["k_done"] == s["k_done"]
+    assert dense.frob(d["X"] - Xs) / dense.frob(Xs) < 1e-13
+    for a, b in zip(d["deltas"][:-1], s["deltas"][:-1]):
+        assert abs(a - b) <= 1e-6 * b + 1e-14
+
+
+def test_spectral_vs_mpmath():
+    """P2: the FP64 scalar iteration matches a 50-digit mpmath recursion of the same algorithm to
+    <= 1e-13 relative, and both match the closed form 1/lam at K = N within the RK4 error."""
+    lams = np.array([0.5, 0.9, 1.3, 2.0, 2.5])
+    N, mG, mF = 4, 1, 16
+    s = spectral.solve(lams, dense.FLOW_INVERSE, 1.0, N, mG, mF, 3)
+    for i, lam in enumerate(lams):
+        x_mp, _ = spectral.mp_parareal_scalar(lam, dense.FLOW_INVERSE, 1, N, mG, mF, 3)
+        assert abs(s["X"][i] - float(x_mp)) <= 1e-13 * abs(float(x_mp))
+    sN = spectral.solve(lams, dense.FLOW_INVERSE, 1.0, N, mG, mF, N)
+    np.testing.assert_allclose(sN["X"], 1.0 / lams, rtol=1e-6)
+
+
+def test_mpmath_golden():
+    """Stored 50-digit values (tests/golden/scalar_parareal_mp50.txt, written by
+    tools/make_golden.py which calls only oracle/) still match the FP64 scalar oracle."""
+    g = _read_golden("scalar_parareal_mp50.txt")
+    for key, val in g.items():
+        flow, lam, N, mG, mF, K = key.split(":")
+        s = spectral.solve(np.array([float(lam)]), int(flow), 1.0 if int(flow) == 0 else 4.0,
+                           int(N), int(mG), int(mF), int(K))
+        assert abs(s["X"][0] - float(val)) <= 1e-13 * abs(float(val)), key
+
+
+def test_diagonal_closed_form_cfg_spectra():
+    """P2 closed form q(1) = 1/lam: sequential fine RK4 with each config's (N, m_F) reaches
+    1/lam within the RK4 error (<= 1e-12 relative) over each config's spectral interval."""
+    for (N, mF, lo, hi) in [(8, 64, 0.5, 1.5), (16, 128, 1.0, 2.0), (64, 256, 0.1, 10.0), (64, 128, 1.0, 3.2)]:
+        lam = np.linspace(lo, hi, 9)
+        s = spectral.solve(lam, dense.FLOW_INVERSE, 1.0, N, 1, mF, N)
+        np.testing.assert_allclose(s["X"], 1.0 / lam, rtol=1e-12)
+
+
+def test_config_workloads_shapes():
+    """workloads builds what BASELINE.json names (sizes, symmetry, spectra)."""
+    for i in (0, 1, 2):
+        w = workloads.config(i)
+        assert w.A.shape == (w.n, w.n) and w.A.flags.c_contiguous
+        assert np.array_equal(w.A, w.A.T)
+        lam = np.linalg.eigvalsh(w.A)
+        assert np.allclose(np.sort(lam), np.sort(w.eigvals), rtol=1e-12, atol=1e-12)
+    assert workloads.config(1).n == 256 and workloads.config(2).n == 1024
