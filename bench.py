@@ -1,0 +1,286 @@
+"""bench.py -- parareal matrix-function solve on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl mine|reference]
+
+Workload (BASELINE.json configs[4], the n = 4096 time-to-tol config that fits one GPU in a
+few-minute run): steady-state square-root flow F(X) = A - X^2, X0 = I, A = 2D 5-point Laplacian
+on a 64 x 64 grid + I (n = 4096, dense FP64), T = 20, N = 64 slices, fine RK4 h = 5/512 (m_F = 32),
+coarse 2 Euler steps/slice, until ||A - X^2||_F/||A||_F <= 1e-10 (checked for k >= 1, reading R10).
+A "step" is one complete parareal solve (Step 0 coarse sweep, fine sweep(s), correction sweep(s),
+stop metric): the whole hot path of SURVEY §8(a).  --config 3 selects the n = 4096 inverse flow
+(much longer: ~20 min per solve on one GPU).
+
+value = algorithmic fine-propagator flops of the solve (8 n^3 per RK4 step x m_F x slice-solves,
+all ranks) / device time of the solve (max over ranks): FP64 TFLOP/s, whole job.  The solve's
+time-to-tol is ms_per_step.  Inputs are resident in HBM (each matrix 128 MiB; the working set of
+~40 GiB is far larger than L2, so no L2 flush is needed).  e2e = the same metric through the C ABI
+with host buffers: mfode_set_matrix (H2D of A) + mfode_parareal_solve + mfode_get_result (D2H of X).
+roofline = the dominant kernel (the fused RK-stage DMMA GEMM on the fine stream), timed by the
+library with CUDA events around every fine chunk on the stream the kernels run on.
+cpu_baseline = the CPU oracle (oracle/dense.py) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-propagator FP64 TFLOP/s and parareal time-to-tol at n=4096, 1/2/4/8 GPUs"
+UNIT = "TFLOP/s"
+
+
+def fp64_peak():
+    """FP64 tensor (DMMA) peak: MEASURED_PEAKS.json has no FP64 entry, so it is the measured chip
+    peak of the mma.sync.m8n8k4.f64 register-loop probe (tools/fp64_peaks.cu), committed in
+    profiles/fp64_peaks_r01.json; cuBLAS DGEMM at n = 4096 is recorded beside it."""
+    p = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    peak, cublas = 37.0, None
+    try:
+        d = json.load(open(p))
+        vals = [x["tflops"] for x in d["probes"] if x.get("probe") == "dmma_m8n8k4"]
+        peak = max(vals)
+        cublas = [x for x in d["dgemm"] if x["n"] == 4096][0]["tflops_burst"]
+    except Exception:
+        pass
+    return peak, cublas
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    def __init__(self, device=0):
+        self.samples = []
+        self.proc = None
+        self.device = device
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            out = ""
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                self.samples.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+            except (ValueError, IndexError):
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        loaded = sorted(s[0] for s in self.samples)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i, v in enumerate(s[3]) if v.lower() == "active"})
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": max(s[1] for s in self.samples),
+                "power_w_max": max(s[2] for s in self.samples), "samples": len(self.samples), "reasons": reasons}
+
+
+def oracle_sample(w, budget_s=20.0):
+    """The oracle as it stands on a bounded sample of the workload: fine RK4 steps of slice 0
+    (oracle.dense.rk4 with the flow's right-hand side), repeated until ~budget_s of CPU work.
+    Returns (tflops, seconds, steps, threads)."""
+    import numpy as np
+    from oracle import dense
+    rhs = dense.make_rhs(w.A, w.flow)
+    X = np.eye(w.n)
+    h = w.T / (w.N * w.m_F)
+    flops_step = (16.0 if w.flow == 0 else 8.0) * float(w.n) ** 3
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        X = dense.rk4(rhs, X, h, 1)
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s * 0.5 or steps >= 64:
+            break
+    dt = time.perf_counter() - t0
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max(i.get("num_threads", 0) for i in threadpool_info()) or None
+    except Exception:
+        pass
+    return flops_step * steps / dt / 1e12, dt, steps, threads or os.cpu_count()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import numpy as np
+    import workloads
+    w = workloads.config(args.config, with_eig=False)
+
+    if args.impl == "reference":
+        # The reference arm is the CPU oracle (no reference implementation exists); rank 0 only.
+        if rank != 0:
+            return 0
+        vals, secs = [], []
+        for i in range(args.warmup + args.steps):
+            tf, dt, steps, threads = oracle_sample(w, budget_s=min(20.0, 120.0 / max(1, args.warmup + args.steps)))
+            if i >= args.warmup:
+                vals.append(tf)
+                secs.append(dt)
+        v = float(np.mean(vals))
+        sample = f"{steps} RK4 step(s) of slice 0 of {w.name} with oracle.dense.rk4 (numpy, OpenBLAS threads)"
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.n, "N_slices": w.N, "m_G": w.m_G, "m_F": w.m_F,
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    import paper_1505_07959_b200 as mf
+
+    torch.cuda.set_device(local_rank)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [bytes(torch.cuda.nccl.unique_id()) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    solver = mf.Solver(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, world=world, rank=rank, device=local_rank,
+                       nccl_uid=uid)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        solver.solve(w.K_max, w.tol, w.stop)
+    barrier()
+    infos = []
+    with ClockSampler(local_rank) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            infos.append(solver.solve(w.K_max, w.tol, w.stop))
+        ev1.record()
+        ev1.synchronize()
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    fine_flops = float(np.mean([i["fine_flops"] for i in infos]))   # all ranks' slices (whole job)
+    value = fine_flops / (ms_step * 1e-3) / 1e12
+
+    # dominant kernel: fused RK-stage DMMA GEMM (library-timed on its own stream, this rank)
+    kms = sum(i["fine_kernel_ms"] for i in infos)
+    kfl = sum(i["fine_kernel_flops"] for i in infos)
+    kla = sum(i["fine_kernel_launches"] for i in infos)
+    achieved = kfl / (kms * 1e-3) / 1e12 if kms > 0 else None
+    peak, cublas = fp64_peak()
+    traffic = ncu_traffic()
+
+    # e2e through the C ABI with host buffers (H2D of A and D2H of X inside the timed region)
+    X_host = np.empty((w.n, w.n), dtype=np.float64)
+    A_host = np.ascontiguousarray(w.A)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    e2e_flops = 0.0
+    for _ in range(args.e2e_steps):
+        solver.set_matrix(A_host)
+        inf = solver.solve(w.K_max, w.tol, w.stop)
+        solver.result(X_host)
+        e2e_flops += inf["fine_flops"]
+    e1.record()
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = e2e_flops / (e2e_ms * 1e-3) / 1e12
+    resid = solver.residual()
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            tf, dt, steps, threads = oracle_sample(w, budget_s=20.0)
+            cpu = {"value": tf, "unit": UNIT, "cores": threads, "kind": "oracle",
+                   "sample": f"{steps} RK4 step(s) of slice 0 of {w.name} with oracle.dense.rk4 "
+                             f"(numpy/OpenBLAS), {dt:.1f} s"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.n, "N_slices": w.N, "m_G": w.m_G, "m_F": w.m_F, "T": w.T,
+                       "stop": "residual<=1e-10 (k>=1)" if w.stop == 2 else f"stop={w.stop} tol={w.tol}",
+                       "global_batch": w.N, "parallelism": f"time-slices/{world} ranks",
+                       "l2": "inputs larger than L2 (128 MiB per matrix, ~40 GiB working set); no flush"},
+            "time_to_tol_ms": ms_step,
+            "k_done": infos[-1]["k_done"],
+            "residual": resid,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.e2e_steps,
+                    "h2d_bytes_per_step": 8 * w.n * w.n, "d2h_bytes_per_step": 8 * w.n * w.n},
+            "gpu_launches": int(sum(i["gpu_launches"] for i in infos)),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "kernel": "dgemm_tma_kernel<128,128,2,4,4,EPI_RK> (fused RK4-stage FP64 DMMA GEMM)",
+                         "launches": kla, "kernel_ms": kms,
+                         "peak_source": "measured FP64 DMMA probe (profiles/fp64_peaks_r01.json); "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "cublas_dgemm_4096_tflops": cublas},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

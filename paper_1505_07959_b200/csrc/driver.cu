@@ -1,0 +1,1106 @@
+// Parareal driver and C ABI (include/mfode.h).
+//
+// Algorithm 1 of Chehab & Petcu on dense n x n FP64 matrices, B200-first:
+//   * every propagation is a chain of TMA/DMMA GEMM launches with fused epilogues (gemm.cuh);
+//   * the fine propagations F(U^k_n) of one sweep are batched over slices (blockIdx -> slice) on a
+//     "fine" stream; Step 0 and the sequential correction run on a high-priority "coarse" stream;
+//   * per-slice events let the fine work of slice chunk [ja, jb) start as soon as the coarse
+//     phase has produced its inputs, and let correction step n start as soon as F(U^k_n) exists;
+//     with overlap on, sweep k+1's fine work is enqueued speculatively before the host reads the
+//     stop metric of sweep k, and a device flag set by the metric kernel cancels it if converged;
+//   * U is ping-pong buffered by sweep parity (the correction of sweep k writes U^{k+1} while the
+//     fine work of sweep k may still read U^k); Fk / Gold are single (WAR ordered by events);
+//   * slices n < k are skipped in sweep k (bitwise identical, reading R14);
+//   * ranks own contiguous slice blocks; boundary states move rank g -> g+1 by NCCL send/recv
+//     (one process per GPU) or by cudaMemcpyAsync between logical ranks in one process.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mfode.h"
+#include "internal.h"
+#include "nccl_min.h"
+
+namespace mfode {
+
+static thread_local std::string g_err;
+
+static int set_global_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded at run time from the library torch already loaded (never both 2.27 and 2.28)
+// ---------------------------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allreduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*errstr)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* env = getenv("MFODE_NCCL_LIB");
+  void* h = nullptr;
+  if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+  api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+  api.send = (decltype(api.send))dlsym(h, "ncclSend");
+  api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+  api.bcast = (decltype(api.bcast))dlsym(h, "ncclBroadcast");
+  api.allreduce = (decltype(api.allreduce))dlsym(h, "ncclAllReduce");
+  api.errstr = (decltype(api.errstr))dlsym(h, "ncclGetErrorString");
+  api.ok = api.commInitRank && api.commDestroy && api.send && api.recv && api.bcast && api.allreduce;
+  return api;
+}
+
+// ---------------------------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------------------------
+struct Rank {
+  int id = 0, s0 = 0, s1 = 0, nloc = 0;
+  double* U[2] = {nullptr, nullptr};  // nloc+1 matrices each; local j <-> global slice s0 + j
+  double* Fk = nullptr;               // nloc: F(U^k_n), also the RK state X in place
+  double* Gold = nullptr;             // nloc: G(U^k_n)
+  double *Ya = nullptr, *Yb = nullptr, *W = nullptr, *S = nullptr;  // RK scratch, `cap` each
+  double *Xa = nullptr, *Xb = nullptr, *Wc = nullptr;              // coarse scratch
+  double* partials = nullptr;  // reductions
+  double* metric = nullptr;    // device scalars [4]
+  double* host_metric = nullptr;  // pinned [4]
+  cudaStream_t fine = nullptr, coarse = nullptr;
+  std::vector<cudaEvent_t> evC;   // nloc: coarse-phase step j done
+  std::vector<cudaEvent_t> evF;   // per fine chunk
+  std::vector<int> chunk_of;      // nloc: fine chunk index of slice j (current sweep)
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_fine_end = nullptr, ev_metric = nullptr;
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;
+  bool fine_started = false;
+  // per-chunk timing of the fine GEMM launches (roofline of the dominant kernel)
+  struct ChunkTiming {
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    int iter = 0, launches = 0;
+    double flops = 0.0;
+  };
+  std::vector<ChunkTiming> tpool;
+  int tused = 0;
+};
+
+}  // namespace mfode
+
+struct mfode_ctx {
+  int n = 0, ld = 0, flow = 0, N = 0, mG = 1, mF = 1;
+  double T = 1.0;
+  int world = 1, device = 0;
+  bool nccl_mode = false;
+  int my_rank = 0;           // NCCL mode: this process' rank
+  ncclComm_t comm = nullptr;
+  double* A = nullptr;       // n x ld
+  double* B = nullptr;       // I - A (inverse flow)
+  int* stop_flag = nullptr;  // device
+  int cap = 1;               // fine batch capacity (slices per launch)
+  int tile = 0;              // 0 auto
+  bool overlap = true;
+  int fine_batch_opt = 0;
+  double normA = 0.0;        // ||A||_F
+  std::vector<mfode::Rank> ranks;
+  // result
+  int result_rank = -1;
+  const double* result_ptr = nullptr;
+  bool has_result = false;
+  int last_k = 0;
+  bool seq_mode = false;
+  std::string err;
+  long long launches_at_start = 0;
+};
+
+namespace mfode {
+
+static int fail(mfode_ctx* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(h, x)                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? MFODE_ENOMEM : MFODE_ECUDA, "%s: %s (%s:%d)", #x, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                                 \
+  } while (0)
+
+#define NCCL_TRY(h, x)                                                                       \
+  do {                                                                                       \
+    ncclResult_t r_ = (x);                                                                   \
+    if (r_ != ncclSuccess)                                                                   \
+      return fail(h, MFODE_ENCCL, "%s: nccl error %d (%s)", #x, (int)r_,                     \
+                  nccl().errstr ? nccl().errstr(r_) : "?");                                  \
+  } while (0)
+
+#define TRY(x)              \
+  do {                      \
+    int s_ = (x);           \
+    if (s_ < 0) return s_;  \
+  } while (0)
+
+static inline size_t mat_elems(const mfode_ctx* h) { return (size_t)h->n * h->ld; }
+static inline double* slot(const mfode_ctx* h, double* slab, int j) { return slab + (size_t)j * mat_elems(h); }
+
+static double rk4_flops(const mfode_ctx* h) {
+  const double n3 = (double)h->n * h->n * h->n;
+  return (h->flow == MFODE_FLOW_INVERSE ? 16.0 : 8.0) * n3;
+}
+static double euler_flops(const mfode_ctx* h) {
+  const double n3 = (double)h->n * h->n * h->n;
+  return (h->flow == MFODE_FLOW_INVERSE ? 4.0 : 2.0) * n3;
+}
+
+int partition(int N, int world, int rank, int* first, int* count) {
+  if (N < 1 || world < 1 || rank < 0 || rank >= world || !first || !count) return MFODE_EINVAL;
+  const int base = N / world, rem = N % world;
+  *count = base + (rank < rem ? 1 : 0);
+  *first = rank * base + std::min(rank, rem);
+  return MFODE_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// one GEMM-based step: K = F-operands ... with epilogue
+// ---------------------------------------------------------------------------------------------
+static GemmParams base_params(const mfode_ctx* h, int num_z) {
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = h->n;
+  p.ld = h->ld;
+  p.num_z = num_z;
+  p.alpha = 1.0;
+  p.beta = 0.0;
+  return p;
+}
+
+// rhs GEMM(s) of the flow for batch z: returns via epilogue params; Y operand given as Operand.
+// inverse: W = B Y (EPI_STORE into Wbuf), then K = Y W with epilogue `epi`
+// sqrt:    K = -(Y Y) + A with epilogue `epi`
+static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, int num_z, GemmParams p, int epi,
+                      cudaStream_t st, cudaEvent_t wait_before_second) {
+  const long long me = (long long)mat_elems(h);
+  if (h->flow == MFODE_FLOW_INVERSE) {
+    GemmParams q = base_params(h, num_z);
+    q.Y_out = MatRef{Wbuf, me};
+    q.stop_flag = p.stop_flag;
+    Operand Bop{h->B, 1, 0, 0};
+    CUDA_TRY(h, launch_gemm(EPI_STORE, h->tile, Bop, Y, q, st));
+    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    Operand Wop{Wbuf, Wcount, 0, 1};
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Wop, p, st));
+  } else {
+    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    p.alpha = -1.0;
+    p.beta = 1.0;
+    p.C = MatRef{h->A, 0};
+    CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Y, p, st));
+  }
+  return MFODE_OK;
+}
+
+// Coarse propagator G on one slice (m_G Euler steps) on the rank's coarse stream.
+// Input matrix `in` (an operand), last step writes according to `last_epi`:
+//   EPI_EULER: Xout = g, and Gold (if non-null) = g
+//   EPI_EULER_CORR: Uout = Fk + (g - Gold); Gold = g  (waits `fk_ready` first)
+static int coarse_G(mfode_ctx* h, Rank& R, const double* in_slab, int in_count, int in_idx, int last_epi,
+                    double* Xout, double* Gold, double* Fk, cudaEvent_t fk_ready) {
+  const double hG = h->T / ((double)h->N * h->mG);
+  const long long me = (long long)mat_elems(h);
+  const double* cur_slab = in_slab;
+  int cur_count = in_count, cur_idx = in_idx;
+  for (int i = 0; i < h->mG; ++i) {
+    const bool last = (i == h->mG - 1);
+    GemmParams p = base_params(h, 1);
+    p.h = hG;
+    p.X_in = MatRef{const_cast<double*>(cur_slab) + (size_t)cur_idx * me, 0};
+    double* tmp = (i % 2 == 0) ? R.Xa : R.Xb;
+    int epi;
+    if (!last) {
+      epi = EPI_EULER;
+      p.X_out = MatRef{tmp, 0};
+    } else if (last_epi == EPI_EULER) {
+      epi = EPI_EULER;
+      p.X_out = MatRef{Xout, 0};
+      p.Gold = MatRef{Gold, 0};
+    } else {
+      epi = EPI_EULER_CORR;
+      p.U_out = MatRef{Xout, 0};
+      p.Gold = MatRef{Gold, 0};
+      p.F_in = MatRef{Fk, 0};
+    }
+    Operand Y{cur_slab, cur_count, cur_idx, 0};
+    TRY(flow_gemms(h, Y, R.Wc, 1, 1, p, epi, R.coarse, (last && last_epi == EPI_EULER_CORR) ? fk_ready : nullptr));
+    cur_slab = tmp;
+    cur_count = 1;
+    cur_idx = 0;
+  }
+  return MFODE_OK;
+}
+
+// Fine propagator F on local slices [ja, jb) of rank R (batched), input U[par][j], output Fk[j].
+static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int* stop_flag) {
+  const int Z = jb - ja;
+  const double hF = h->T / ((double)h->N * h->mF);
+  const long long me = (long long)mat_elems(h);
+  Operand Xu{R.U[par], R.nloc + 1, ja, 1};
+  Operand Xf{R.Fk, R.nloc, ja, 1};
+  Operand Ya{R.Ya, h->cap, 0, 1}, Yb{R.Yb, h->cap, 0, 1};
+  for (int i = 0; i < h->mF; ++i) {
+    const Operand& X = (i == 0) ? Xu : Xf;
+    double* Xin = (i == 0) ? slot(h, R.U[par], ja) : slot(h, R.Fk, ja);
+    for (int s = 1; s <= 4; ++s) {
+      GemmParams p = base_params(h, Z);
+      p.stop_flag = stop_flag;
+      p.stage = s;
+      p.h = hF;
+      p.X_in = MatRef{Xin, me};
+      p.S = MatRef{R.S, me};
+      const Operand* Yin;
+      if (s == 1) {
+        Yin = &X;
+        p.Y_out = MatRef{R.Ya, me};
+      } else if (s == 2) {
+        Yin = &Ya;
+        p.Y_out = MatRef{R.Yb, me};
+      } else if (s == 3) {
+        Yin = &Yb;
+        p.Y_out = MatRef{R.Ya, me};
+      } else {
+        Yin = &Ya;
+        p.X_out = MatRef{slot(h, R.Fk, ja), me};
+        p.Y_out = MatRef{nullptr, 0};
+      }
+      TRY(flow_gemms(h, *Yin, R.W, h->cap, Z, p, EPI_RK, R.fine, nullptr));
+    }
+  }
+  return MFODE_OK;
+}
+
+static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
+  if (k >= R.s1) return MFODE_OK;
+  const int ja0 = std::max(0, k - R.s0);
+  const int active = R.nloc - ja0;
+  if (active <= 0) return MFODE_OK;
+  const int nchunks = (active + h->cap - 1) / h->cap;
+  const int size = (active + nchunks - 1) / nchunks;
+  if ((int)R.evF.size() < nchunks) {
+    int old = (int)R.evF.size();
+    R.evF.resize(nchunks);
+    for (int c = old; c < nchunks; ++c) CUDA_TRY(h, cudaEventCreateWithFlags(&R.evF[c], cudaEventDisableTiming));
+  }
+  const int par = k % 2;
+  const int* flag = speculative ? h->stop_flag : nullptr;
+  for (int c = 0; c < nchunks; ++c) {
+    const int ja = ja0 + c * size;
+    const int jb = std::min(R.nloc, ja + size);
+    if (ja >= jb) break;
+    CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.evC[jb - 1], 0));
+    if (!R.fine_started) {
+      CUDA_TRY(h, cudaEventRecord(R.ev_f0, R.fine));
+      R.fine_started = true;
+    }
+    if (R.tused == (int)R.tpool.size()) {
+      R.tpool.emplace_back();
+      CUDA_TRY(h, cudaEventCreate(&R.tpool.back().t0));
+      CUDA_TRY(h, cudaEventCreate(&R.tpool.back().t1));
+    }
+    Rank::ChunkTiming& ct = R.tpool[R.tused++];
+    ct.iter = k;
+    ct.launches = h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
+    ct.flops = (double)(jb - ja) * h->mF * rk4_flops(h);
+    CUDA_TRY(h, cudaEventRecord(ct.t0, R.fine));
+    TRY(fine_chunk(h, R, par, ja, jb, flag));
+    CUDA_TRY(h, cudaEventRecord(ct.t1, R.fine));
+    CUDA_TRY(h, cudaEventRecord(R.evF[c], R.fine));
+    for (int j = ja; j < jb; ++j) R.chunk_of[j] = c;
+  }
+  CUDA_TRY(h, cudaEventRecord(R.ev_f1, R.fine));
+  return MFODE_OK;
+}
+
+// boundary: rank g's U[par][nloc] -> rank g+1's U[par][0]
+static int send_boundary(mfode_ctx* h, Rank& R, int par) {
+  if (R.id >= h->world - 1) return MFODE_OK;
+  if (h->nccl_mode) {
+    NCCL_TRY(h, nccl().send(slot(h, R.U[par], R.nloc), mat_elems(h), ncclFloat64, R.id + 1, h->comm, R.coarse));
+  } else {
+    // logical ranks: the receiver copies after the sender's event (recorded in evC[nloc-1])
+  }
+  return MFODE_OK;
+}
+
+static int recv_boundary(mfode_ctx* h, Rank& R, int par) {
+  if (R.id == 0) return MFODE_OK;
+  if (h->nccl_mode) {
+    NCCL_TRY(h, nccl().recv(R.U[par], mat_elems(h), ncclFloat64, R.id - 1, h->comm, R.coarse));
+  } else {
+    Rank& P = h->ranks[R.id - 1];
+    CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, P.evC[P.nloc - 1], 0));
+    CUDA_TRY(h, cudaMemcpyAsync(R.U[par], slot(h, P.U[par], P.nloc), mat_elems(h) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, R.coarse));
+  }
+  return MFODE_OK;
+}
+
+static int enqueue_step0(mfode_ctx* h, Rank& R) {
+  TRY(recv_boundary(h, R, 0));
+  for (int j = 0; j < R.nloc; ++j) {
+    TRY(coarse_G(h, R, R.U[0], R.nloc + 1, j, EPI_EULER, slot(h, R.U[0], j + 1), slot(h, R.Gold, j), nullptr,
+                 nullptr));
+    CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
+  }
+  TRY(send_boundary(h, R, 0));
+  return MFODE_OK;
+}
+
+static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
+  if (k >= R.s1) return MFODE_OK;
+  const int cur = k % 2, nxt = (k + 1) % 2;
+  const int j0 = std::max(0, k - R.s0);
+  if (k < R.s0) TRY(recv_boundary(h, R, nxt));
+  for (int j = j0; j < R.nloc; ++j) {
+    const double* in_slab;
+    int in_idx;
+    if (j == j0 && k >= R.s0) {
+      in_slab = R.U[cur];
+      in_idx = j0;
+    } else {
+      in_slab = R.U[nxt];
+      in_idx = j;
+    }
+    TRY(coarse_G(h, R, in_slab, R.nloc + 1, in_idx, EPI_EULER_CORR, slot(h, R.U[nxt], j + 1), slot(h, R.Gold, j),
+                 slot(h, R.Fk, j), R.evF[R.chunk_of[j]]));
+    CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
+  }
+  TRY(send_boundary(h, R, nxt));
+  return MFODE_OK;
+}
+
+// flow residual of X (device, on rank R's coarse stream) into R.metric[idx]
+static int enqueue_residual(mfode_ctx* h, Rank& R, const double* slab, int count, int idx, int out_idx, double tol,
+                            int* flag) {
+  const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, 1);
+  GemmParams p = base_params(h, 1);
+  p.partials = R.partials;
+  const long long ntiles = gemm_tiles(tile, h->n, 1);
+  double denom;
+  if (h->flow == MFODE_FLOW_INVERSE) {
+    p.shift = 1.0;
+    Operand Aop{h->A, 1, 0, 0};
+    Operand Xop{slab, count, idx, 0};
+    CUDA_TRY(h, launch_gemm(EPI_RESID, tile, Aop, Xop, p, R.coarse));
+    denom = sqrt((double)h->n);
+  } else {
+    p.alpha = -1.0;
+    p.beta = 1.0;
+    p.C = MatRef{h->A, 0};
+    Operand Xop{slab, count, idx, 0};
+    CUDA_TRY(h, launch_gemm(EPI_RESID, tile, Xop, Xop, p, R.coarse));
+    denom = h->normA;
+  }
+  CUDA_TRY(h, launch_reduce_partials(R.partials, (int)ntiles, denom, R.metric + out_idx, tol, flag, R.coarse));
+  return MFODE_OK;
+}
+
+static int alloc_rank(mfode_ctx* h, Rank& R) {
+  const size_t me = mat_elems(h) * sizeof(double);
+  CUDA_TRY(h, cudaMalloc(&R.U[0], me * (R.nloc + 1)));
+  CUDA_TRY(h, cudaMalloc(&R.U[1], me * (R.nloc + 1)));
+  CUDA_TRY(h, cudaMalloc(&R.Fk, me * std::max(1, R.nloc)));
+  CUDA_TRY(h, cudaMalloc(&R.Gold, me * std::max(1, R.nloc)));
+  CUDA_TRY(h, cudaMalloc(&R.Ya, me * h->cap));
+  CUDA_TRY(h, cudaMalloc(&R.Yb, me * h->cap));
+  CUDA_TRY(h, cudaMalloc(&R.S, me * h->cap));
+  if (h->flow == MFODE_FLOW_INVERSE) CUDA_TRY(h, cudaMalloc(&R.W, me * h->cap));
+  CUDA_TRY(h, cudaMalloc(&R.Xa, me));
+  CUDA_TRY(h, cudaMalloc(&R.Xb, me));
+  CUDA_TRY(h, cudaMalloc(&R.Wc, me));
+  const long long maxtiles = std::max<long long>(gemm_tiles(TILE_32, h->n, 1), kFrobPartials);
+  CUDA_TRY(h, cudaMalloc(&R.partials, sizeof(double) * (maxtiles + 16)));
+  CUDA_TRY(h, cudaMalloc(&R.metric, sizeof(double) * 8));
+  CUDA_TRY(h, cudaMallocHost(&R.host_metric, sizeof(double) * 8));
+  // zero everything once: padding columns stay zero forever (kernels never write them)
+  CUDA_TRY(h, cudaMemset(R.U[0], 0, me * (R.nloc + 1)));
+  CUDA_TRY(h, cudaMemset(R.U[1], 0, me * (R.nloc + 1)));
+  CUDA_TRY(h, cudaMemset(R.Fk, 0, me * std::max(1, R.nloc)));
+  CUDA_TRY(h, cudaMemset(R.Gold, 0, me * std::max(1, R.nloc)));
+  CUDA_TRY(h, cudaMemset(R.Ya, 0, me * h->cap));
+  CUDA_TRY(h, cudaMemset(R.Yb, 0, me * h->cap));
+  CUDA_TRY(h, cudaMemset(R.S, 0, me * h->cap));
+  if (R.W) CUDA_TRY(h, cudaMemset(R.W, 0, me * h->cap));
+  CUDA_TRY(h, cudaMemset(R.Xa, 0, me));
+  CUDA_TRY(h, cudaMemset(R.Xb, 0, me));
+  CUDA_TRY(h, cudaMemset(R.Wc, 0, me));
+  int lo, hi;
+  CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CUDA_TRY(h, cudaStreamCreateWithPriority(&R.fine, cudaStreamNonBlocking, lo));
+  CUDA_TRY(h, cudaStreamCreateWithPriority(&R.coarse, cudaStreamNonBlocking, hi));
+  R.evC.resize(std::max(1, R.nloc));
+  for (auto& e : R.evC) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  R.chunk_of.assign(std::max(1, R.nloc), 0);
+  CUDA_TRY(h, cudaEventCreate(&R.ev_t0));
+  CUDA_TRY(h, cudaEventCreate(&R.ev_t1));
+  CUDA_TRY(h, cudaEventCreate(&R.ev_f0));
+  CUDA_TRY(h, cudaEventCreate(&R.ev_f1));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&R.ev_fine_end, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&R.ev_metric, cudaEventDisableTiming));
+  return MFODE_OK;
+}
+
+static void free_rank(mfode_ctx* h, Rank& R) {
+  double* bufs[] = {R.U[0], R.U[1], R.Fk, R.Gold, R.Ya, R.Yb, R.W, R.S, R.Xa, R.Xb, R.Wc, R.partials, R.metric};
+  const size_t me = mat_elems(h);
+  for (double* b : bufs)
+    if (b) {
+      forget_maps(b, b + me * (size_t)(std::max(R.nloc, h->cap) + 2));
+      cudaFree(b);
+    }
+  if (R.host_metric) cudaFreeHost(R.host_metric);
+  if (R.fine) cudaStreamDestroy(R.fine);
+  if (R.coarse) cudaStreamDestroy(R.coarse);
+  for (auto e : R.evC) cudaEventDestroy(e);
+  for (auto e : R.evF) cudaEventDestroy(e);
+  for (auto& ct : R.tpool) {
+    cudaEventDestroy(ct.t0);
+    cudaEventDestroy(ct.t1);
+  }
+  cudaEvent_t evs[] = {R.ev_t0, R.ev_t1, R.ev_f0, R.ev_f1, R.ev_fine_end, R.ev_metric};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+}
+
+// A (device, leading dim ld_src) -> h->A (ld), B = I - A, ||A||_F
+static int load_matrix(mfode_ctx* h, const double* src, bool host, size_t ld_src, cudaStream_t st) {
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->A, h->ld * sizeof(double), src, ld_src * sizeof(double), h->n * sizeof(double),
+                                h->n, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+  if (h->B) CUDA_TRY(h, launch_i_minus(h->B, h->A, h->n, h->ld, st));
+  Rank& R = h->ranks[0];
+  CUDA_TRY(h, launch_frob(h->A, nullptr, h->n, h->ld, R.partials, R.metric, 1, 0.0, nullptr, st));
+  CUDA_TRY(h, cudaMemcpyAsync(R.host_metric, R.metric, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  h->normA = R.host_metric[1];
+  h->has_result = false;
+  return MFODE_OK;
+}
+
+static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, int flow, double T, int N, int mG,
+                       int mF, const mfode_dist* dist, cudaStream_t user_stream) {
+  if (!out) return set_global_err(MFODE_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!A) return set_global_err(MFODE_EINVAL, "A is NULL");
+  if (n < 1 || n > 65536) return set_global_err(MFODE_EINVAL, "n=%lld out of range [1, 65536]", (long long)n);
+  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT) return set_global_err(MFODE_EINVAL, "unknown flow %d", flow);
+  if (!(T > 0.0) || !std::isfinite(T)) return set_global_err(MFODE_EINVAL, "T must be finite and > 0");
+  if (N < 1 || mG < 1 || mF < 1) return set_global_err(MFODE_EINVAL, "N, coarse_steps, fine_steps must be >= 1");
+  int world = dist ? dist->world : 1;
+  if (world < 1 || world > N) return set_global_err(MFODE_EINVAL, "world=%d must be in [1, N=%d]", world, N);
+  std::unique_ptr<mfode_ctx> h(new mfode_ctx());
+  h->n = (int)n;
+  h->ld = (int)((n + 15) / 16 * 16);
+  h->flow = flow;
+  h->T = T;
+  h->N = N;
+  h->mG = mG;
+  h->mF = mF;
+  h->world = world;
+  int dev = 0;
+  if (dist) dev = dist->device;
+  else cudaGetDevice(&dev);
+  h->device = dev;
+  if (cudaSetDevice(dev) != cudaSuccess) return set_global_err(MFODE_ECUDA, "cudaSetDevice(%d) failed", dev);
+  h->nccl_mode = dist && dist->nccl_uid && world > 1;
+  if (h->nccl_mode) {
+    if (dist->rank < 0 || dist->rank >= world) return set_global_err(MFODE_EINVAL, "rank out of range");
+    h->my_rank = dist->rank;
+    if (!nccl().ok) return set_global_err(MFODE_ENCCL, "NCCL library not available (set MFODE_NCCL_LIB)");
+    ncclUniqueId uid;
+    memcpy(&uid, dist->nccl_uid, sizeof(uid));
+    ncclResult_t r = nccl().commInitRank(&h->comm, world, uid, dist->rank);
+    if (r != ncclSuccess) return set_global_err(MFODE_ENCCL, "ncclCommInitRank failed: %d", (int)r);
+  }
+  // fine batch capacity: enough batched tiles to fill the chip, bounded by the slice count
+  {
+    const int nloc_max = (N + world - 1) / world;
+    const int t128 = (int)gemm_tiles(TILE_128, h->n, 1);
+    int cap = std::max(1, (int)((8LL * 148 + t128 - 1) / t128));
+    if (h->n <= 512) cap = nloc_max;   // small matrices: batch every slice of the rank
+    h->cap = std::min(cap, nloc_max);
+  }
+  // ranks
+  const int nranks_here = h->nccl_mode ? 1 : world;
+  h->ranks.resize(nranks_here);
+  for (int i = 0; i < nranks_here; ++i) {
+    Rank& R = h->ranks[i];
+    R.id = h->nccl_mode ? h->my_rank : i;
+    int first, count;
+    partition(N, world, R.id, &first, &count);
+    R.s0 = first;
+    R.s1 = first + count;
+    R.nloc = count;
+  }
+  mfode_ctx* hp = h.get();
+  const size_t me = mat_elems(hp) * sizeof(double);
+  if (cudaMalloc(&hp->A, me) != cudaSuccess) return set_global_err(MFODE_ENOMEM, "alloc A failed");
+  cudaMemset(hp->A, 0, me);
+  if (flow == MFODE_FLOW_INVERSE) {
+    if (cudaMalloc(&hp->B, me) != cudaSuccess) return set_global_err(MFODE_ENOMEM, "alloc B failed");
+    cudaMemset(hp->B, 0, me);
+  }
+  if (cudaMalloc(&hp->stop_flag, sizeof(int)) != cudaSuccess) return set_global_err(MFODE_ENOMEM, "alloc flag failed");
+  cudaMemset(hp->stop_flag, 0, sizeof(int));
+  for (auto& R : hp->ranks) {
+    int s = alloc_rank(hp, R);
+    if (s < 0) {
+      std::string e = hp->err;
+      mfode_destroy(h.release());
+      return set_global_err(s, "%s", e.c_str());
+    }
+  }
+  // X0 = I in slot 0 of both U buffers of rank 0 (logical or NCCL), once
+  for (auto& R : hp->ranks)
+    if (R.id == 0) {
+      launch_identity(R.U[0], hp->n, hp->ld, 1, 0, R.coarse);
+      launch_identity(R.U[1], hp->n, hp->ld, 1, 0, R.coarse);
+    }
+  cudaStream_t st = hp->ranks[0].coarse;
+  if (!host && user_stream != (cudaStream_t)-1) {
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, user_stream);
+    cudaStreamWaitEvent(st, ev, 0);
+    cudaEventDestroy(ev);
+  }
+  int s = load_matrix(hp, A, host, (size_t)n, st);
+  if (s < 0) {
+    std::string e = hp->err;
+    mfode_destroy(h.release());
+    return set_global_err(s, "%s", e.c_str());
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    mfode_destroy(h.release());
+    return set_global_err(MFODE_ECUDA, "create: device error");
+  }
+  *out = h.release();
+  return MFODE_OK;
+}
+
+static Rank& last_rank(mfode_ctx* h) { return h->ranks.back(); }
+static bool owns_last(mfode_ctx* h) { return last_rank(h).id == h->world - 1; }
+
+// host-visible broadcast of metric[idx] from the last rank (NCCL) -> every rank's host_metric[idx]
+static int fetch_metric(mfode_ctx* h, int idx, int count) {
+  Rank& L = last_rank(h);
+  if (h->nccl_mode) {
+    NCCL_TRY(h, nccl().bcast(L.metric + idx, L.metric + idx, count, ncclFloat64, h->world - 1, h->comm, L.coarse));
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(L.host_metric + idx, L.metric + idx, count * sizeof(double), cudaMemcpyDeviceToHost,
+                              L.coarse));
+  CUDA_TRY(h, cudaEventRecord(L.ev_metric, L.coarse));
+  return MFODE_OK;
+}
+
+static int first_bad_slice(mfode_ctx* h) {
+  // scan U (latest buffers) of every local rank for non-finite entries; -1 if none
+  for (auto& R : h->ranks) {
+    for (int j = 0; j <= R.nloc; ++j) {
+      const int gidx = R.s0 + j;
+      const int par = (gidx <= h->last_k ? gidx : h->last_k) % 2;
+      launch_frob(slot(h, R.U[par], j), nullptr, h->n, h->ld, R.partials, R.metric + 6, 1, 0.0, nullptr, R.coarse);
+      cudaMemcpyAsync(R.host_metric + 6, R.metric + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, R.coarse);
+      cudaStreamSynchronize(R.coarse);
+      if (!std::isfinite(R.host_metric[7])) return gidx;
+    }
+  }
+  return -1;
+}
+
+static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
+  if (K_max < 0 || !(tol >= 0.0) || stop < 0 || stop > 2) return fail(h, MFODE_EINVAL, "bad K_max/tol/stop");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const long long L0 = g_launches.load();
+  const int K_eff = std::min(K_max, h->N);
+  mfode_solve_info loc;
+  memset(&loc, 0, sizeof(loc));
+  loc.bad_slice = -1;
+  loc.last_delta = NAN;
+  loc.world = h->world;
+  for (int i = 0; i < 64; ++i) loc.deltas[i] = NAN;
+  h->seq_mode = false;
+  h->has_result = false;
+  // start: every stream waits for the previous work of this handle (serialised solves)
+  for (auto& R : h->ranks) {
+    CUDA_TRY(h, cudaStreamSynchronize(R.fine));
+    CUDA_TRY(h, cudaStreamSynchronize(R.coarse));
+  }
+  Rank& L = last_rank(h);
+  CUDA_TRY(h, cudaMemsetAsync(h->stop_flag, 0, sizeof(int), h->ranks[0].coarse));
+  CUDA_TRY(h, cudaStreamSynchronize(h->ranks[0].coarse));
+  for (auto& R : h->ranks) {
+    R.fine_started = false;
+    R.tused = 0;
+    CUDA_TRY(h, cudaEventRecord(R.ev_t0, R.coarse));
+    CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_t0, 0));
+  }
+  // ---- Step 0 ----
+  for (auto& R : h->ranks) TRY(enqueue_step0(h, R));
+  double res0 = NAN;
+  if (stop == MFODE_STOP_RESIDUAL && owns_last(h)) TRY(enqueue_residual(h, L, L.U[0], L.nloc + 1, L.nloc, 1, 0.0, nullptr));
+  if (stop == MFODE_STOP_RESIDUAL) {
+    TRY(fetch_metric(h, 1, 1));
+    CUDA_TRY(h, cudaEventSynchronize(L.ev_metric));
+    res0 = L.host_metric[1];
+  }
+  loc.residual0 = res0;
+  int k_done = 0;
+  bool converged = (stop == MFODE_STOP_FIXED_K);
+  int status = MFODE_OK;
+  const bool spec = h->overlap && stop != MFODE_STOP_FIXED_K;
+  if (K_eff > 0)
+    for (auto& R : h->ranks) TRY(enqueue_fine(h, R, 0, false));
+  for (int k = 0; k < K_eff; ++k) {
+    for (auto& R : h->ranks) TRY(enqueue_correction(h, R, k));
+    // stop metric on the last rank: delta of U_N (always), residual (STOP_RESIDUAL)
+    const int nxt = (k + 1) % 2, cur = k % 2;
+    int* flag = nullptr;
+    if (owns_last(h)) {
+      flag = (stop == MFODE_STOP_DELTA && spec && !h->nccl_mode) ? h->stop_flag : nullptr;
+      CUDA_TRY(h, launch_frob(slot(h, L.U[nxt], L.nloc), slot(h, L.U[cur], L.nloc), h->n, h->ld, L.partials,
+                              L.metric + 0, 0, tol, flag, L.coarse));
+      if (stop == MFODE_STOP_RESIDUAL) {
+        int* rflag = (spec && !h->nccl_mode) ? h->stop_flag : nullptr;
+        TRY(enqueue_residual(h, L, L.U[nxt], L.nloc + 1, L.nloc, 1, tol, rflag));
+      }
+    }
+    TRY(fetch_metric(h, 0, 2));
+    if (spec && h->nccl_mode) {
+      // every rank sets its own flag from the broadcast metric
+      for (auto& R : h->ranks)
+        CUDA_TRY(h, launch_copy_flag(R.metric + (stop == MFODE_STOP_DELTA ? 0 : 1), tol, h->stop_flag, R.coarse));
+    }
+    const bool more = (k + 1 < K_eff);
+    if (more && (spec || stop == MFODE_STOP_FIXED_K))
+      for (auto& R : h->ranks) TRY(enqueue_fine(h, R, k + 1, spec));
+    CUDA_TRY(h, cudaEventSynchronize(L.ev_metric));
+    const double delta = L.host_metric[0];
+    const double resid = L.host_metric[1];
+    k_done = k + 1;
+    h->last_k = k_done;
+    loc.last_delta = delta;
+    if (k < 64) loc.deltas[k] = delta;
+    if (!std::isfinite(delta) || (stop == MFODE_STOP_RESIDUAL && !std::isfinite(resid))) {
+      status = MFODE_ENONFINITE;
+      break;
+    }
+    if (stop == MFODE_STOP_DELTA && delta <= tol) {
+      converged = true;
+      break;
+    }
+    if (stop == MFODE_STOP_RESIDUAL && resid <= tol) {
+      converged = true;
+      break;
+    }
+    if (k_done == h->N) {  // R15: U^N = sequential fine, exact
+      converged = true;
+      break;
+    }
+    if (more && !(spec || stop == MFODE_STOP_FIXED_K))
+      for (auto& R : h->ranks) TRY(enqueue_fine(h, R, k + 1, false));
+  }
+  if (K_eff == 0) h->last_k = 0;
+  if (k_done == h->N) converged = true;
+  // join: the coarse stream waits for (possibly cancelled) speculative fine work
+  for (auto& R : h->ranks) {
+    CUDA_TRY(h, cudaEventRecord(R.ev_fine_end, R.fine));
+    CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, R.ev_fine_end, 0));
+    CUDA_TRY(h, cudaEventRecord(R.ev_t1, R.coarse));
+  }
+  double ms_max = 0.0;
+  for (auto& R : h->ranks) {
+    CUDA_TRY(h, cudaEventSynchronize(R.ev_t1));
+    float ms = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&ms, R.ev_t0, R.ev_t1));
+    ms_max = std::max(ms_max, (double)ms);
+  }
+  if (h->nccl_mode) {
+    // max over ranks of the device time
+    L.host_metric[5] = ms_max;
+    CUDA_TRY(h, cudaMemcpyAsync(L.metric + 5, L.host_metric + 5, sizeof(double), cudaMemcpyHostToDevice, L.coarse));
+    NCCL_TRY(h, nccl().allreduce(L.metric + 5, L.metric + 5, 1, ncclFloat64, ncclMax, h->comm, L.coarse));
+    CUDA_TRY(h, cudaMemcpyAsync(L.host_metric + 5, L.metric + 5, sizeof(double), cudaMemcpyDeviceToHost, L.coarse));
+    CUDA_TRY(h, cudaStreamSynchronize(L.coarse));
+    ms_max = L.host_metric[5];
+  }
+  if (L.fine_started) {
+    float fms = 0.f;
+    if (cudaEventElapsedTime(&fms, L.ev_f0, L.ev_f1) == cudaSuccess) loc.ms_fine = fms;
+  }
+  loc.ms_total = ms_max;
+  loc.k_done = k_done;
+  for (auto& R : h->ranks)
+    for (int i = 0; i < R.tused; ++i) {
+      const Rank::ChunkTiming& ct = R.tpool[i];
+      if (ct.iter >= k_done) continue;   // cancelled speculative sweep
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ct.t0, ct.t1) == cudaSuccess) {
+        loc.fine_kernel_ms += ms;
+        loc.fine_kernel_launches += ct.launches;
+        loc.fine_kernel_flops += ct.flops;
+      }
+    }
+  loc.converged = converged ? 1 : 0;
+  // flops: slice-solves of the sweeps actually used (all ranks)
+  double slice_solves = 0.0;
+  for (int k = 0; k < k_done; ++k) slice_solves += (double)(h->N - k);
+  double corr_slices = 0.0;
+  for (int k = 0; k < k_done; ++k) corr_slices += (double)(h->N - k);
+  loc.fine_flops = slice_solves * h->mF * rk4_flops(h);
+  loc.coarse_flops = (h->N + corr_slices) * h->mG * euler_flops(h);
+  loc.gpu_launches = (int)(g_launches.load() - L0);
+  // result
+  h->result_rank = h->world - 1;
+  h->result_ptr = owns_last(h) ? slot(h, L.U[k_done % 2], L.nloc) : nullptr;
+  h->has_result = true;
+  if (status == MFODE_ENONFINITE) {
+    loc.bad_slice = first_bad_slice(h);
+  } else if (owns_last(h) || h->nccl_mode) {
+    double r = NAN;
+    if (stop == MFODE_STOP_RESIDUAL && k_done > 0) {
+      r = L.host_metric[1];
+    } else if (stop == MFODE_STOP_RESIDUAL && k_done == 0) {
+      r = res0;
+    }
+    loc.residual = r;
+  }
+  if (info) *info = loc;
+  if (status < 0) return fail(h, status, "non-finite state (first bad slice %d)", loc.bad_slice);
+  if (!converged) {
+    h->err = "not converged within K_max sweeps";
+    return MFODE_NOT_CONVERGED;
+  }
+  return MFODE_OK;
+}
+
+static int sequential_impl(mfode_ctx* h, mfode_solve_info* info) {
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const long long L0 = g_launches.load();
+  for (auto& R : h->ranks) {
+    CUDA_TRY(h, cudaStreamSynchronize(R.fine));
+    CUDA_TRY(h, cudaStreamSynchronize(R.coarse));
+    CUDA_TRY(h, cudaEventRecord(R.ev_t0, R.coarse));
+  }
+  const int saved_cap = h->cap;
+  for (auto& R : h->ranks) {
+    // S_{s0} arrives from the previous rank; each slice: Fk_j = F(S_j) on the coarse stream, S_{j+1} = Fk_j
+    TRY(recv_boundary(h, R, 0));
+    std::swap(R.fine, R.coarse);  // run the fine chunks on the coarse stream (strictly sequential)
+    h->cap = 1;
+    int s = MFODE_OK;
+    for (int j = 0; j < R.nloc && s == MFODE_OK; ++j) {
+      s = fine_chunk(h, R, 0, j, j + 1, nullptr);
+      if (s == MFODE_OK) {
+        cudaError_t e = cudaMemcpyAsync(slot(h, R.U[0], j + 1), slot(h, R.Fk, j), mat_elems(h) * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, R.fine);
+        if (e != cudaSuccess) s = fail(h, MFODE_ECUDA, "copy: %s", cudaGetErrorString(e));
+      }
+    }
+    std::swap(R.fine, R.coarse);
+    h->cap = saved_cap;
+    TRY(s);
+    if (R.nloc > 0) CUDA_TRY(h, cudaEventRecord(R.evC[R.nloc - 1], R.coarse));
+    TRY(send_boundary(h, R, 0));
+    CUDA_TRY(h, cudaEventRecord(R.ev_t1, R.coarse));
+  }
+  double ms_max = 0.0;
+  for (auto& R : h->ranks) {
+    CUDA_TRY(h, cudaEventSynchronize(R.ev_t1));
+    float ms = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&ms, R.ev_t0, R.ev_t1));
+    ms_max = std::max(ms_max, (double)ms);
+  }
+  h->seq_mode = true;
+  h->last_k = 0;
+  Rank& L = last_rank(h);
+  h->result_rank = h->world - 1;
+  h->result_ptr = owns_last(h) ? slot(h, L.U[0], L.nloc) : nullptr;
+  h->has_result = true;
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->k_done = 0;
+    info->bad_slice = -1;
+    info->converged = 1;
+    info->world = h->world;
+    info->last_delta = NAN;
+    info->residual = NAN;
+    info->residual0 = NAN;
+    info->ms_total = ms_max;
+    info->fine_flops = (double)h->N * h->mF * rk4_flops(h);
+    info->gpu_launches = (int)(g_launches.load() - L0);
+    for (int i = 0; i < 64; ++i) info->deltas[i] = NAN;
+  }
+  return MFODE_OK;
+}
+
+}  // namespace mfode
+
+using namespace mfode;
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+int mfode_create(mfode_ctx** out, const double* A, int64_t n, int flow, double T, int N_slices, int coarse_steps,
+                 int fine_steps, const mfode_dist* dist) {
+  return create_impl(out, A, true, n, flow, T, N_slices, coarse_steps, fine_steps, dist, (cudaStream_t)-1);
+}
+
+int mfode_create_device(mfode_ctx** out, const double* dA, int64_t n, int flow, double T, int N_slices,
+                        int coarse_steps, int fine_steps, const mfode_dist* dist, void* cuda_stream) {
+  return create_impl(out, dA, false, n, flow, T, N_slices, coarse_steps, fine_steps, dist, (cudaStream_t)cuda_stream);
+}
+
+int mfode_set_matrix(mfode_ctx* h, const double* A) {
+  if (!h || !A) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (cudaSetDevice(h->device) != cudaSuccess) return fail(h, MFODE_ECUDA, "cudaSetDevice");
+  for (auto& R : h->ranks) {
+    cudaStreamSynchronize(R.fine);
+    cudaStreamSynchronize(R.coarse);
+  }
+  return load_matrix(h, A, true, (size_t)h->n, h->ranks[0].coarse);
+}
+
+int mfode_parareal_solve(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
+  if (!h) return set_global_err(MFODE_EINVAL, "NULL handle");
+  return solve_impl(h, K_max, tol, stop, info);
+}
+
+int mfode_sequential_fine(mfode_ctx* h, mfode_solve_info* info) {
+  if (!h) return set_global_err(MFODE_EINVAL, "NULL handle");
+  return sequential_impl(h, info);
+}
+
+int mfode_residual(mfode_ctx* h, double* rel) {
+  if (!h || !rel) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (!h->has_result) return fail(h, MFODE_EINVAL, "no result yet (call a solve first)");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  Rank& L = last_rank(h);
+  if (owns_last(h)) {
+    TRY(enqueue_residual(h, L, h->result_ptr, 1, 0, 2, 0.0, nullptr));
+  }
+  TRY(fetch_metric(h, 2, 1));
+  CUDA_TRY(h, cudaEventSynchronize(L.ev_metric));
+  *rel = L.host_metric[2];
+  return MFODE_OK;
+}
+
+static int get_result_impl(mfode_ctx* h, double* dst, bool host, cudaStream_t user) {
+  if (!h || !dst) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (!h->has_result) return fail(h, MFODE_EINVAL, "no result yet (call a solve first)");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  Rank& L = last_rank(h);
+  const double* src = h->result_ptr;
+  if (h->nccl_mode) {
+    // broadcast the result from the last rank into this rank's Xa scratch
+    double* buf = L.Xa;
+    if (owns_last(h)) CUDA_TRY(h, cudaMemcpyAsync(buf, src, mat_elems(h) * sizeof(double), cudaMemcpyDeviceToDevice, L.coarse));
+    NCCL_TRY(h, nccl().bcast(buf, buf, mat_elems(h), ncclFloat64, h->world - 1, h->comm, L.coarse));
+    src = buf;
+  }
+  CUDA_TRY(h, cudaMemcpy2DAsync(dst, h->n * sizeof(double), src, h->ld * sizeof(double), h->n * sizeof(double), h->n,
+                                host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, L.coarse));
+  if (host) {
+    CUDA_TRY(h, cudaStreamSynchronize(L.coarse));
+  } else {
+    cudaEvent_t ev;
+    CUDA_TRY(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaEventRecord(ev, L.coarse);
+    cudaStreamWaitEvent(user, ev, 0);
+    cudaEventDestroy(ev);
+  }
+  return MFODE_OK;
+}
+
+int mfode_get_result(mfode_ctx* h, double* X) { return get_result_impl(h, X, true, nullptr); }
+
+int mfode_get_result_device(mfode_ctx* h, double* dX, void* stream) {
+  return get_result_impl(h, dX, false, (cudaStream_t)stream);
+}
+
+int mfode_get_slice(mfode_ctx* h, int n_index, double* U) {
+  if (!h || !U) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (n_index < 0 || n_index > h->N) return fail(h, MFODE_EINVAL, "slice %d out of range", n_index);
+  if (!h->has_result) return fail(h, MFODE_EINVAL, "no solve yet");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  for (auto& R : h->ranks) {
+    // U_n is stored by the rank with s0 <= n <= s1 (n == s1 also as the next rank's boundary)
+    if (n_index < R.s0 || n_index > R.s1) continue;
+    const int j = n_index - R.s0;
+    const int par = h->seq_mode ? 0 : ((n_index <= h->last_k ? n_index : h->last_k) % 2);
+    CUDA_TRY(h, cudaMemcpy2DAsync(U, h->n * sizeof(double), slot(h, R.U[par], j), h->ld * sizeof(double),
+                                  h->n * sizeof(double), h->n, cudaMemcpyDeviceToHost, R.coarse));
+    CUDA_TRY(h, cudaStreamSynchronize(R.coarse));
+    return MFODE_OK;
+  }
+  return fail(h, MFODE_EINVAL, "slice %d not owned by this rank", n_index);
+}
+
+int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
+  if (!h || !key) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (!strcmp(key, "overlap")) {
+    h->overlap = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "tile")) {
+    if (value < 0 || value > 3) return fail(h, MFODE_EINVAL, "tile must be 0..3");
+    h->tile = (int)value;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "fine_batch")) {
+    // shrinking only (scratch is allocated at create for the automatic capacity)
+    int nloc_max = 0;
+    for (auto& R : h->ranks) nloc_max = std::max(nloc_max, R.nloc);
+    if (value < 0) return fail(h, MFODE_EINVAL, "fine_batch must be >= 0");
+    if (value == 0) return MFODE_OK;
+    if (value > h->cap) return fail(h, MFODE_EINVAL, "fine_batch %lld exceeds allocated capacity %d", (long long)value, h->cap);
+    h->cap = (int)value;
+    return MFODE_OK;
+  }
+  return fail(h, MFODE_EINVAL, "unknown option '%s'", key);
+}
+
+const char* mfode_last_error(const mfode_ctx* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+void mfode_destroy(mfode_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (auto& R : h->ranks) free_rank(h, R);
+  const size_t me = mat_elems(h);
+  if (h->A) {
+    forget_maps(h->A, h->A + me);
+    cudaFree(h->A);
+  }
+  if (h->B) {
+    forget_maps(h->B, h->B + me);
+    cudaFree(h->B);
+  }
+  if (h->stop_flag) cudaFree(h->stop_flag);
+  if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
+  delete h;
+}
+
+// ---- kernel-level ----------------------------------------------------------------------------
+int mfode_dgemm(const double* dA, const double* dB, const double* dC, double* dD, int64_t n, int64_t ld, double alpha,
+                double beta, int tile, void* stream) {
+  if (!dA || !dB || !dD || (beta != 0.0 && !dC)) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (n < 1 || ld < n || (ld * 8) % 16 != 0 || tile < 0 || tile > 3)
+    return set_global_err(MFODE_EINVAL, "bad n/ld/tile");
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = (int)n;
+  p.ld = (int)ld;
+  p.num_z = 1;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.C = MatRef{const_cast<double*>(dC), 0};
+  p.Y_out = MatRef{dD, 0};
+  Operand A{dA, 1, 0, 0}, B{dB, 1, 0, 0};
+  cudaError_t e = launch_gemm(EPI_STORE, tile, A, B, p, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "dgemm: %s", cudaGetErrorString(e));
+  return MFODE_OK;
+}
+
+int mfode_rk_stage(const double* dYop, const double* dBop, const double* dC, double alpha, double beta, double* dX,
+                   double* dS, double* dYnext, int stage, double h, int64_t n, int64_t ld, int tile, void* stream) {
+  if (!dYop || !dBop || !dX || !dS || (stage < 4 && !dYnext) || (beta != 0.0 && !dC))
+    return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (stage < 1 || stage > 4 || n < 1 || ld < n || (ld * 8) % 16 != 0 || tile < 0 || tile > 3)
+    return set_global_err(MFODE_EINVAL, "bad stage/n/ld/tile");
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = (int)n;
+  p.ld = (int)ld;
+  p.num_z = 1;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.C = MatRef{const_cast<double*>(dC), 0};
+  p.X_in = MatRef{dX, 0};
+  p.X_out = MatRef{dX, 0};
+  p.S = MatRef{dS, 0};
+  p.Y_out = MatRef{stage < 4 ? dYnext : nullptr, 0};
+  p.stage = stage;
+  p.h = h;
+  Operand A{dYop, 1, 0, 0}, B{dBop, 1, 0, 0};
+  cudaError_t e = launch_gemm(EPI_RK, tile, A, B, p, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "rk_stage: %s", cudaGetErrorString(e));
+  return MFODE_OK;
+}
+
+int mfode_frobenius(const double* dX, const double* dY, int64_t n, int64_t ld, double* out, void* stream) {
+  if (!dX || !out) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (n < 1 || ld < n || ld % 2 != 0) return set_global_err(MFODE_EINVAL, "bad n/ld");
+  cudaStream_t st = (cudaStream_t)stream;
+  double *part = nullptr, *res = nullptr;
+  if (cudaMallocAsync(&part, sizeof(double) * kFrobPartials, st) != cudaSuccess ||
+      cudaMallocAsync(&res, sizeof(double) * 2, st) != cudaSuccess)
+    return set_global_err(MFODE_ENOMEM, "frobenius scratch");
+  // Note: padding columns (ld > n) are included; callers keep them zero or pass ld == n.
+  cudaError_t e = launch_frob(dX, dY, (int)n, (int)ld, part, res, 1, 0.0, nullptr, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, res, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(res, st);
+  if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "frobenius: %s", cudaGetErrorString(e));
+  return MFODE_OK;
+}
+
+int mfode_partition(int N, int world, int rank, int* first, int* count) {
+  int s = partition(N, world, rank, first, count);
+  if (s != MFODE_OK) return set_global_err(s, "bad partition arguments");
+  return MFODE_OK;
+}
+
+int64_t mfode_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+const char* mfode_last_global_error(void) { return g_err.c_str(); }
+
+const char* mfode_version(void) { return "mfode 0.1 (sm_100a, FP64 DMMA + TMA)"; }
+
+}  // extern "C"

@@ -1,0 +1,375 @@
+// FP64 DMMA GEMM for sm_100a with TMA-staged, 128B-swizzled tiles and fused parareal epilogues.
+//
+// Computes, for every batch index z of a launch, K_z = alpha * Aop_z * Bop_z (+ beta * C_z) on
+// n x n row-major matrices and applies one of the epilogues of the parareal hot path
+// (DESIGN.md "Kernels"):
+//   EPI_STORE       D = K                                   (W = B Y: first GEMM of F(Y) = Y (B Y))
+//   EPI_RK          classical-RK4 stage combination, s = 1..4 (reading R1):
+//                     s=1: S = K;      Y' = X + (h/2) K
+//                     s=2: S = S + 2K; Y' = X + (h/2) K
+//                     s=3: S = S + 2K; Y' = X + h K
+//                     s=4: X = X + (h/6) (S + K)   [S = ((k1 + 2k2) + 2k3) + k4]
+//   EPI_EULER       g = X + h K -> Xout (and Gold if given)            (coarse step)
+//   EPI_EULER_CORR  g = X + h K; U = Fk + (g - Gold); Gold = g          (eq. eqStepk+1; R3)
+//   EPI_RESID       per-tile partial sum of (K - shift*I)^2             (residual norms)
+//
+// FP64 on B200 has no tcgen05 kind (ptxas rejects kind::f64) and no wgmma, so the tensor path is
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, measured 37.0 TF/s chip peak).  Structure:
+//   * persistent CTAs, static round-robin tile schedule over (z, tile_m, tile_n);
+//   * one producer warp: one elected lane issues cp.async.bulk.tensor (TMA) loads of a
+//     BM x 16 A tile and BN/16 16x16 B boxes per k-step into a STAGES-deep mbarrier ring,
+//     128B swizzle (so fragment loads are bank-conflict free, see below);
+//   * WARPS_M x WARPS_N consumer warps: register-resident accumulators (warp tile WM x WN),
+//     fragments read with 128-bit ld.shared, 2 k-steps of DMMA per 16-byte fragment;
+//   * epilogue straight from registers: each lane owns 4 consecutive columns of a row per 16-col
+//     group, so stores are 2 x 16 B per (row, group); fused element-wise parareal arithmetic.
+// Fragment/swizzle mapping (bank-conflict free for 128-bit loads):
+//   A tile (row r, k) lives at r*128 + (((k>>1) ^ (r&7)) << 4) + (k&1)*8.  Lane (g=lane>>2, c=lane&3)
+//   loads 16 B at chunk (4kb + c) of row 8mt + rho(g): values for k = 8kb+2c+s, s = 0,1.
+//   rho = {0,4,1,5,2,6,3,7} puts the two rows of each quarter-warp in different swizzle halves.
+//   B box (16 k-rows x 16 cols) at k*128 + (((j>>1) ^ (k&7)) << 4) + (j&1)*8: lane loads the
+//   16 B pair (cols 2g, 2g+1) of row k = 8kb+2c+s, feeding two n-tiles (even / odd columns).
+//   The k-order inside a 16-wide k-step is thus permuted identically for A and B (exact sums are
+//   unchanged; the rounding order is fixed for a given n, independent of batch and slice).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+
+namespace mfode {
+
+enum Epi : int { EPI_STORE = 0, EPI_RK = 1, EPI_EULER = 2, EPI_EULER_CORR = 3, EPI_RESID = 4 };
+
+struct MatRef {           // element (z, r, c) at p[z * zstride + r * ld + c]
+  double* p;
+  long long zstride;
+  __host__ __device__ double* at(int z) const { return p + (long long)z * zstride; }
+};
+
+struct GemmParams {
+  int n, ld, num_z;
+  int a_base, a_step;     // A-operand slice in its tensor map: a_base + z * a_step
+  int b_base, b_step;
+  double alpha, beta;     // K = alpha * acc + beta * C
+  MatRef C;               // read iff beta != 0
+  MatRef X_in, X_out, S, Y_out, F_in, Gold, U_out;
+  int stage;              // RK stage 1..4
+  double h;
+  double shift;           // EPI_RESID: subtract shift * I
+  double* partials;       // EPI_RESID: one double per tile (index z * tiles + tile)
+  const int* stop_flag;   // if non-null and set: the launch does nothing
+};
+
+constexpr int BK = 16;    // k-depth of one pipeline stage (16 doubles = one 128-byte swizzle row)
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+struct GemmCfg {
+  static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
+  // Register budget: the register file is split over the 4 SM sub-partitions (16K regs each) and
+  // warps are assigned round-robin, so 8 consumer warps + 1 producer warp (3 warps on one SMSP)
+  // cap every thread at 168 registers.  The 8-warp config therefore uses a whole producer
+  // warpgroup and setmaxnreg: producers drop to 40 registers, consumers grow to 232.
+  static constexpr bool kSetMaxNReg = (kConsumerWarps % 4 == 0) && (kConsumerWarps >= 8);
+  static constexpr int kProducerWarps = kSetMaxNReg ? 4 : 1;
+  static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
+  static constexpr int WM = BM / WARPS_M;
+  static constexpr int WN = BN / WARPS_N;
+  static constexpr int MT = WM / 8;          // 8-row m-tiles per warp
+  static constexpr int NG = WN / 16;         // 16-column groups per warp (2 n-tiles each)
+  static constexpr int kABytes = BM * BK * 8;
+  static constexpr int kBBytes = BN * BK * 8;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8;
+  static_assert(WM % 8 == 0 && WN % 16 == 0, "warp tile must be a multiple of 8 x 16");
+  static_assert(BM <= 256 && BN % 16 == 0, "TMA box limits");
+};
+
+__device__ __forceinline__ int rho8(int g) { return ((g & 1) << 2) | (g >> 1); }
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int EPI>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmParams p) {
+  using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>;
+  if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
+  uint64_t* empty = full + STAGES;
+  double* red = reinterpret_cast<double*>(empty + STAGES);   // EPI_RESID cross-warp scratch
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n = p.n;
+  const int tiles_m = (n + BM - 1) / BM;
+  const int tiles_n = (n + BN - 1) / BN;
+  const int tiles_per_z = tiles_m * tiles_n;
+  const int total = tiles_per_z * p.num_z;
+  const int KT = (n + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::kConsumerWarps);
+    }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  __syncthreads();
+
+  if constexpr (Cfg::kSetMaxNReg) {
+    if (warp >= Cfg::kConsumerWarps)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  }
+
+  if (warp >= Cfg::kConsumerWarps) {
+    // ===================== TMA producer (one elected lane) =====================
+    if (warp == Cfg::kConsumerWarps && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int z = t / tiles_per_z;
+        const int r = t - z * tiles_per_z;
+        const int m0 = (r / tiles_n) * BM;
+        const int n0 = (r % tiles_n) * BN;
+        const int sa = p.a_base + z * p.a_step;
+        const int sb = p.b_base + z * p.b_step;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char* sA = smem + stage * Cfg::kStageBytes;
+          unsigned char* sB = sA + Cfg::kABytes;
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_3d(sA, &tmA, &full[stage], kt * BK, m0, sa);
+#pragma unroll
+          for (int g = 0; g < BN / 16; ++g) tma_load_3d(sB + g * 2048, &tmB, &full[stage], n0 + g * 16, kt * BK, sb);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ===================== consumers: DMMA main loop + fused epilogue =====================
+  const int wm = warp / WARPS_N;
+  const int wn = warp % WARPS_N;
+  const int g = lane >> 2;
+  const int c = lane & 3;
+  const int rowA = rho8(g);
+  int stage = 0;
+  uint32_t phase = 0;
+  const uint32_t smem_base = smem_u32(smem);
+
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int z = t / tiles_per_z;
+    const int r = t - z * tiles_per_z;
+    const int m0 = (r / tiles_n) * BM;
+    const int n0 = (r % tiles_n) * BN;
+
+    double acc[Cfg::MT][2 * Cfg::NG][2];
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < 2 * Cfg::NG; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
+      const uint32_t sB = sA + Cfg::kABytes;
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        double2 af[Cfg::MT];
+#pragma unroll
+        for (int mt = 0; mt < Cfg::MT; ++mt) {
+          const int row = wm * Cfg::WM + mt * 8 + rowA;   // row & 7 == rowA
+          af[mt] = lds128(sA + row * 128 + ((((kb << 2) + c) ^ rowA) << 4));
+        }
+        double2 bf[Cfg::NG][2];
+#pragma unroll
+        for (int ng = 0; ng < Cfg::NG; ++ng) {
+          const int grp = (wn * Cfg::WN) / 16 + ng;
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int k = kb * 8 + 2 * c + s;
+            bf[ng][s] = lds128(sB + grp * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int mt = 0; mt < Cfg::MT; ++mt) {
+            const double a = s ? af[mt].y : af[mt].x;
+#pragma unroll
+            for (int ng = 0; ng < Cfg::NG; ++ng) {
+              dmma(acc[mt][2 * ng][0], acc[mt][2 * ng][1], a, bf[ng][s].x);
+              dmma(acc[mt][2 * ng + 1][0], acc[mt][2 * ng + 1][1], a, bf[ng][s].y);
+            }
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+
+    // ---------------- epilogue ----------------
+    double part = 0.0;
+    const int ld = p.ld;
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt) {
+      const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
+      if (row >= n) continue;
+#pragma unroll
+      for (int ng = 0; ng < Cfg::NG; ++ng) {
+        const int col = n0 + wn * Cfg::WN + ng * 16 + 4 * c;
+        if (col >= n) continue;
+        double k4[4] = {acc[mt][2 * ng][0], acc[mt][2 * ng + 1][0], acc[mt][2 * ng][1], acc[mt][2 * ng + 1][1]};
+        const long long off = (long long)row * ld + col;
+        const bool full4 = (col + 3 < n);
+        const int cnt = full4 ? 4 : (n - col);
+        // K = alpha*acc + beta*C
+        if (p.beta != 0.0) {
+          const double* Cp = p.C.at(z) + off;
+          if (full4) {
+            const double2 c0 = *reinterpret_cast<const double2*>(Cp);
+            const double2 c1 = *reinterpret_cast<const double2*>(Cp + 2);
+            k4[0] = fma(p.alpha, k4[0], p.beta * c0.x);
+            k4[1] = fma(p.alpha, k4[1], p.beta * c0.y);
+            k4[2] = fma(p.alpha, k4[2], p.beta * c1.x);
+            k4[3] = fma(p.alpha, k4[3], p.beta * c1.y);
+          } else {
+            #pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < cnt) k4[e] = fma(p.alpha, k4[e], p.beta * Cp[e]);
+          }
+        } else if (p.alpha != 1.0) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) k4[e] *= p.alpha;
+        }
+        double in0[4] = {0, 0, 0, 0}, in1[4] = {0, 0, 0, 0}, o0[4] = {0, 0, 0, 0}, o1[4] = {0, 0, 0, 0};
+        if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o0[e] = k4[e];
+        } else if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (e < cnt) {
+              const double v = k4[e] - ((row == col + e) ? p.shift : 0.0);
+              part = fma(v, v, part);
+            }
+          }
+        } else {
+          // load X (and S / Fk / Gold as needed)
+          const double* Xp = p.X_in.at(z) + off;
+          if (full4) {
+            const double2 a0 = *reinterpret_cast<const double2*>(Xp);
+            const double2 a1 = *reinterpret_cast<const double2*>(Xp + 2);
+            in0[0] = a0.x; in0[1] = a0.y; in0[2] = a1.x; in0[3] = a1.y;
+          } else {
+            #pragma unroll
+            for (int e = 0; e < 4; ++e) in0[e] = (e < cnt) ? Xp[e] : 0.0;
+          }
+          const double* Sp = nullptr;
+          if constexpr (EPI == EPI_RK) Sp = p.S.at(z) + off;
+          if constexpr (EPI == EPI_EULER_CORR) Sp = p.Gold.at(z) + off;
+          if constexpr (EPI == EPI_RK || EPI == EPI_EULER_CORR) {
+            if (EPI == EPI_EULER_CORR || p.stage > 1) {
+              if (full4) {
+                const double2 a0 = *reinterpret_cast<const double2*>(Sp);
+                const double2 a1 = *reinterpret_cast<const double2*>(Sp + 2);
+                in1[0] = a0.x; in1[1] = a0.y; in1[2] = a1.x; in1[3] = a1.y;
+              } else {
+                #pragma unroll
+                for (int e = 0; e < 4; ++e) in1[e] = (e < cnt) ? Sp[e] : 0.0;
+              }
+            }
+          }
+          if constexpr (EPI == EPI_RK) {
+            const double h = p.h;
+            const int st = p.stage;
+            if (st == 4) {
+              const double h6 = h / 6.0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) o0[e] = fma(h6, in1[e] + k4[e], in0[e]);   // X
+            } else {
+              const double cy = (st == 3) ? h : 0.5 * h;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o1[e] = (st == 1) ? k4[e] : fma(2.0, k4[e], in1[e]);                // S
+                o0[e] = fma(cy, k4[e], in0[e]);                                      // Y'
+              }
+            }
+          } else if constexpr (EPI == EPI_EULER) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o0[e] = fma(p.h, k4[e], in0[e]);
+          } else if constexpr (EPI == EPI_EULER_CORR) {
+            const double* Fp = p.F_in.at(z) + off;
+            double fk[4];
+            if (full4) {
+              const double2 a0 = *reinterpret_cast<const double2*>(Fp);
+              const double2 a1 = *reinterpret_cast<const double2*>(Fp + 2);
+              fk[0] = a0.x; fk[1] = a0.y; fk[2] = a1.x; fk[3] = a1.y;
+            } else {
+              #pragma unroll
+              for (int e = 0; e < 4; ++e) fk[e] = (e < cnt) ? Fp[e] : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const double gnew = fma(p.h, k4[e], in0[e]);
+              o1[e] = gnew;                         // Gold <- G(U^{k+1}_n)
+              o0[e] = fk[e] + (gnew - in1[e]);      // U^{k+1}_{n+1} = F + (Gnew - Gold)   (R3)
+            }
+          }
+        }
+        // ---- stores ----
+        auto store4 = [&](double* dst, const double* v) {
+          if (full4) {
+            *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+            *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < cnt) dst[e] = v[e];
+          }
+        };
+        if constexpr (EPI == EPI_STORE) {
+          store4(p.Y_out.at(z) + off, o0);
+        } else if constexpr (EPI == EPI_RK) {
+          if (p.stage == 4) {
+            store4(p.X_out.at(z) + off, o0);
+            if (p.Y_out.p) store4(p.Y_out.at(z) + off, o0);
+          } else {
+            store4(p.S.at(z) + off, o1);
+            store4(p.Y_out.at(z) + off, o0);
+          }
+        } else if constexpr (EPI == EPI_EULER) {
+          store4(p.X_out.at(z) + off, o0);
+          if (p.Gold.p) store4(p.Gold.at(z) + off, o0);
+        } else if constexpr (EPI == EPI_EULER_CORR) {
+          store4(p.U_out.at(z) + off, o0);
+          store4(p.Gold.at(z) + off, o1);
+        }
+      }
+    }
+    if constexpr (EPI == EPI_RESID) {
+      // deterministic tile reduction: fixed shuffle tree, then warps in index order
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      named_bar_sync(1, Cfg::kConsumerWarps * 32);
+      if (lane == 0) red[warp] = part;
+      named_bar_sync(1, Cfg::kConsumerWarps * 32);
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < Cfg::kConsumerWarps; ++w) s += red[w];
+        p.partials[t] = s;
+      }
+    }
+  }
+}
+
+}  // namespace mfode

@@ -1,0 +1,39 @@
+// Internal declarations shared by kernels.cu and driver.cu (not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+#include "gemm.cuh"
+
+namespace mfode {
+
+enum Tile : int { TILE_AUTO = 0, TILE_128 = 1, TILE_64 = 2, TILE_32 = 3 };
+
+// A GEMM operand: matrix `base + z * step` of a slab of `count` n x n matrices at `slab`.
+struct Operand {
+  const double* slab;
+  int count;
+  int base;
+  int step;
+};
+
+extern std::atomic<long long> g_launches;
+
+cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st);
+cudaError_t launch_i_minus(double* B, const double* A, int n, int ld, cudaStream_t st);
+// mode 0: out[0] = ||X-Y||/||X||; mode 1: out[0] = ||X-Y||, out[1] = ||X||.  partials: 2*296 doubles.
+cudaError_t launch_frob(const double* X, const double* Y, int n, int ld, double* partials, double* out, int mode,
+                        double tol, int* stop_flag, cudaStream_t st);
+cudaError_t launch_reduce_partials(const double* partials, int count, double denom, double* out, double tol,
+                                   int* stop_flag, cudaStream_t st);
+cudaError_t launch_copy_flag(const double* metric, double tol, int* stop_flag, cudaStream_t st);
+cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
+int choose_tile(int n, int num_z);
+long long gemm_tiles(int tile, int n, int num_z);
+void forget_maps(const double* lo, const double* hi);
+
+constexpr int kFrobPartials = 2 * 296;
+
+}  // namespace mfode

@@ -1,0 +1,336 @@
+// Device kernels of the parareal hot path other than the GEMM main loop, and the GEMM launcher.
+//   K3 setup:        X = I, B = I - A                      (X0 = I; R2)
+//   K5 reductions:   ||X - Y||_F, ||X||_F, residual partial sums -> one scalar, deterministic
+//                    (fixed grid, fixed shuffle tree, fixed-order final pass; no FP atomics)
+//   stop flag:       flag = (metric <= tol) for speculative-work cancellation
+//   GEMM launcher:   TMA tensor-map cache + tile-config dispatch of gemm.cuh
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "gemm.cuh"
+#include "internal.h"
+
+namespace mfode {
+
+std::atomic<long long> g_launches{0};
+
+// --------------------------------------------------------------------------------------------
+// Element-wise kernels (HBM-bound; 16-byte vector accesses; padding columns kept at zero)
+// --------------------------------------------------------------------------------------------
+__global__ void k_identity(double* X, int n, int ld, int count, long long zstride) {
+  const long long per = (long long)n * ld;
+  const long long total = per * count;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; i < total;
+       i += (long long)gridDim.x * blockDim.x * 2) {
+    const long long z = i / per;
+    const long long e = i - z * per;
+    const int r = (int)(e / ld), c = (int)(e - (long long)r * ld);
+    double2 v;
+    v.x = (r == c && c < n) ? 1.0 : 0.0;
+    v.y = (r == c + 1 && c + 1 < n) ? 1.0 : 0.0;
+    *reinterpret_cast<double2*>(X + z * zstride + e) = v;
+  }
+}
+
+__global__ void k_i_minus(double* B, const double* A, int n, int ld) {
+  const long long total = (long long)n * ld;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; i < total;
+       i += (long long)gridDim.x * blockDim.x * 2) {
+    const int r = (int)(i / ld), c = (int)(i - (long long)r * ld);
+    const double2 a = *reinterpret_cast<const double2*>(A + i);
+    double2 v;
+    v.x = (c < n) ? ((r == c ? 1.0 : 0.0) - a.x) : 0.0;
+    v.y = (c + 1 < n) ? ((r == c + 1 ? 1.0 : 0.0) - a.y) : 0.0;
+    *reinterpret_cast<double2*>(B + i) = v;
+  }
+}
+
+// partials[b] = (sum (X-Y)^2, sum X^2) over block b's fixed share; Y may be null.
+constexpr int kRedBlocks = 296;
+constexpr int kRedThreads = 256;
+
+__global__ void __launch_bounds__(kRedThreads) k_frob_partial(const double* X, const double* Y,
+                                                              long long total, double* partials) {
+  double d = 0.0, x = 0.0;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; i < total;
+       i += (long long)gridDim.x * blockDim.x * 2) {
+    const double2 a = *reinterpret_cast<const double2*>(X + i);
+    double2 b = make_double2(0.0, 0.0);
+    if (Y) b = *reinterpret_cast<const double2*>(Y + i);
+    const double e0 = a.x - b.x, e1 = a.y - b.y;
+    d = fma(e0, e0, d);
+    d = fma(e1, e1, d);
+    x = fma(a.x, a.x, x);
+    x = fma(a.y, a.y, x);
+  }
+  __shared__ double sd[kRedThreads / 32], sx[kRedThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sd[threadIdx.x >> 5] = d;
+    sx[threadIdx.x >> 5] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) {
+      a += sd[w];
+      b += sx[w];
+    }
+    partials[2 * blockIdx.x] = a;
+    partials[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// Fixed-order final reduction of `count` interleaved pairs (stride 2) or singles (stride 1).
+// mode 0 (delta): out = sqrt(sum0)/sqrt(sum1) ; mode 1 (norms): out[0] = sqrt(sum0), out[1] = sqrt(sum1)
+// mode 2 (residual): out = sqrt(sum)/denom
+__global__ void k_reduce_final(const double* partials, int count, int stride, int mode, double denom,
+                               double* out, double tol, int* stop_flag) {
+  __shared__ double s0[32], s1[32];
+  // fixed order: thread t sums indices t, t+blockDim, ... ; then a fixed warp tree; then warps in order
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    a += partials[(long long)i * stride];
+    if (stride == 2) b += partials[(long long)i * stride + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s0[threadIdx.x >> 5] = a;
+    s1[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      x += s0[w];
+      y += s1[w];
+    }
+    double metric;
+    if (mode == 0) {
+      metric = sqrt(x) / sqrt(y);
+      out[0] = metric;
+    } else if (mode == 1) {
+      out[0] = sqrt(x);
+      out[1] = sqrt(y);
+      metric = out[0];
+    } else {
+      metric = sqrt(x) / denom;
+      out[0] = metric;
+    }
+    if (stop_flag) *stop_flag = (metric <= tol) ? 1 : 0;
+  }
+}
+
+__global__ void k_copy_flag(const double* metric, double tol, int* stop_flag) {
+  *stop_flag = (*metric <= tol) ? 1 : 0;
+}
+
+// --------------------------------------------------------------------------------------------
+// host wrappers
+// --------------------------------------------------------------------------------------------
+static int ew_grid(long long elems) {
+  long long g = (elems / 2 + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  k_identity<<<ew_grid((long long)n * ld * count), 256, 0, st>>>(X, n, ld, count, zstride);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_i_minus(double* B, const double* A, int n, int ld, cudaStream_t st) {
+  k_i_minus<<<ew_grid((long long)n * ld), 256, 0, st>>>(B, A, n, ld);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frob(const double* X, const double* Y, int n, int ld, double* partials, double* out,
+                        int mode, double tol, int* stop_flag, cudaStream_t st) {
+  const long long total = (long long)n * ld;
+  k_frob_partial<<<kRedBlocks, kRedThreads, 0, st>>>(X, Y, total, partials);
+  k_reduce_final<<<1, 1024, 0, st>>>(partials, kRedBlocks, 2, mode, 1.0, out, tol, stop_flag);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_partials(const double* partials, int count, double denom, double* out,
+                                   double tol, int* stop_flag, cudaStream_t st) {
+  k_reduce_final<<<1, 1024, 0, st>>>(partials, count, 1, 2, denom, out, tol, stop_flag);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_flag(const double* metric, double tol, int* stop_flag, cudaStream_t st) {
+  k_copy_flag<<<1, 1, 0, st>>>(metric, tol, stop_flag);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------------------------
+// TMA tensor maps
+// --------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// slab = `count` n x n matrices of leading dimension ld, matrix s at base + s * n * ld.
+bool encode_slab_map(CUtensorMap* m, const double* base, int n, int ld, int count, int box_rows) {
+  PFN_encodeTiled enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)count};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)n * ld * 8};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct MapCache {
+  std::mutex mu;
+  std::map<std::tuple<const double*, int, int, int, int>, CUtensorMap> maps;
+};
+static MapCache& map_cache() {
+  static MapCache c;
+  return c;
+}
+
+static bool get_map(CUtensorMap* out, const double* base, int n, int ld, int count, int box_rows) {
+  auto& c = map_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto key = std::make_tuple(base, n, ld, count, box_rows);
+  auto it = c.maps.find(key);
+  if (it != c.maps.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (!encode_slab_map(out, base, n, ld, count, box_rows)) return false;
+  if (c.maps.size() > 4096) c.maps.clear();
+  c.maps[key] = *out;
+  return true;
+}
+
+void forget_maps(const double* lo, const double* hi) {
+  auto& c = map_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  for (auto it = c.maps.begin(); it != c.maps.end();) {
+    const double* b = std::get<0>(it->first);
+    if (b >= lo && b < hi)
+      it = c.maps.erase(it);
+    else
+      ++it;
+  }
+}
+
+// --------------------------------------------------------------------------------------------
+// GEMM dispatch
+// --------------------------------------------------------------------------------------------
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int BM, int BN, int WM_, int WN_, int ST, int EPI>
+static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, cudaStream_t st) {
+  using Cfg = GemmCfg<BM, BN, WM_, WN_, ST>;
+  auto kern = dgemm_tma_kernel<BM, BN, WM_, WN_, ST, EPI>;
+  static int occ = -1;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads, Cfg::kSmemBytes);
+    occ = o > 0 ? o : 1;
+  });
+  const long long tiles = (long long)((p.n + BM - 1) / BM) * ((p.n + BN - 1) / BN) * p.num_z;
+  long long grid = (long long)num_sms() * occ;
+  if (grid > tiles) grid = tiles;
+  kern<<<(unsigned)grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(ma, mb, p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+int tile_box_rows(int tile) { return tile == TILE_128 ? 128 : (tile == TILE_64 ? 64 : 32); }
+
+int choose_tile(int n, int num_z) {
+  auto tiles = [&](int bm, int bn) { return (long long)((n + bm - 1) / bm) * ((n + bn - 1) / bn) * num_z; };
+  const int sms = num_sms();
+  if (tiles(128, 128) >= 2LL * sms) return TILE_128;
+  if (tiles(64, 64) >= (long long)sms) return TILE_64;
+  return TILE_32;
+}
+
+long long gemm_tiles(int tile, int n, int num_z) {
+  const int bm = tile_box_rows(tile), bn = (tile == TILE_128) ? 128 : 64;
+  return (long long)((n + bm - 1) / bm) * ((n + bn - 1) / bn) * num_z;
+}
+
+template <int EPI>
+static cudaError_t dispatch_tile(int tile, const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
+                                 cudaStream_t st) {
+  switch (tile) {
+    case TILE_128: return launch_cfg<128, 128, 2, 4, 4, EPI>(ma, mb, p, st);
+    case TILE_64: return launch_cfg<64, 64, 2, 2, 4, EPI>(ma, mb, p, st);
+    default: return launch_cfg<32, 64, 1, 2, 4, EPI>(ma, mb, p, st);
+  }
+}
+
+cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st) {
+  if (tile == TILE_AUTO) tile = choose_tile(p.n, p.num_z);
+  CUtensorMap ma, mb;
+  if (!get_map(&ma, A.slab, p.n, p.ld, A.count, tile_box_rows(tile))) return cudaErrorInvalidValue;
+  if (!get_map(&mb, B.slab, p.n, p.ld, B.count, 16)) return cudaErrorInvalidValue;
+  p.a_base = A.base;
+  p.a_step = A.step;
+  p.b_base = B.base;
+  p.b_step = B.step;
+  switch (epi) {
+    case EPI_STORE: return dispatch_tile<EPI_STORE>(tile, ma, mb, p, st);
+    case EPI_RK: return dispatch_tile<EPI_RK>(tile, ma, mb, p, st);
+    case EPI_EULER: return dispatch_tile<EPI_EULER>(tile, ma, mb, p, st);
+    case EPI_EULER_CORR: return dispatch_tile<EPI_EULER_CORR>(tile, ma, mb, p, st);
+    case EPI_RESID: return dispatch_tile<EPI_RESID>(tile, ma, mb, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mfode

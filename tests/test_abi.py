@@ -1,0 +1,87 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/mfode.h declares,
+and the host-only logic (partition, argument validation before any CUDA call) behaves."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1505_07959_b200 as mf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "mfode.h")).read()
+    return sorted(set(re.findall(r"MFODE_API\s+[\w\s\*]*?\b(mfode_\w+)\s*\(", src)))
+
+
+def test_library_builds_and_loads():
+    from paper_1505_07959_b200 import build
+    build.build(verbose=False)
+    L = mf.lib()
+    assert "sm_100a" in mf.version()
+
+
+def test_exports_every_declared_symbol():
+    L = mf.lib()
+    names = _declared()
+    assert len(names) >= 19
+    for name in names:
+        assert hasattr(L, name), name
+    assert sorted(names) == sorted(mf.EXPORTED)
+
+
+def test_partition_blocks():
+    for N in (1, 7, 16, 64):
+        for world in range(1, min(N, 8) + 1):
+            covered = []
+            sizes = []
+            for r in range(world):
+                f, c = mf.partition(N, world, r)
+                covered.extend(range(f, f + c))
+                sizes.append(c)
+            assert covered == list(range(N))
+            assert max(sizes) - min(sizes) <= 1
+            assert sizes == sorted(sizes, reverse=True)
+
+
+def test_partition_invalid():
+    with pytest.raises(mf.MfodeError):
+        mf.partition(4, 5, 0) if False else mf.partition(0, 1, 0)
+    with pytest.raises(mf.MfodeError):
+        mf.partition(8, 2, 2)
+
+
+def test_create_rejects_bad_arguments_without_gpu():
+    """Argument validation happens before any CUDA call, so it is checkable on a CPU box."""
+    L = mf.lib()
+    h = ctypes.c_void_p()
+    A = np.eye(4)
+    assert L.mfode_create(ctypes.byref(h), None, 4, 0, 1.0, 4, 1, 1, None) == mf.EINVAL
+    assert L.mfode_create(ctypes.byref(h), A.ctypes.data, 0, 0, 1.0, 4, 1, 1, None) == mf.EINVAL
+    assert L.mfode_create(ctypes.byref(h), A.ctypes.data, 4, 9, 1.0, 4, 1, 1, None) == mf.EINVAL
+    assert L.mfode_create(ctypes.byref(h), A.ctypes.data, 4, 0, -1.0, 4, 1, 1, None) == mf.EINVAL
+    assert L.mfode_create(ctypes.byref(h), A.ctypes.data, 4, 0, 1.0, 0, 1, 1, None) == mf.EINVAL
+    assert L.mfode_create(ctypes.byref(h), A.ctypes.data, 4, 0, 1.0, 4, 0, 1, None) == mf.EINVAL
+    d = mf.Dist(0, 9, 0, None)
+    assert L.mfode_create(ctypes.byref(h), A.ctypes.data, 4, 0, 1.0, 4, 1, 1, ctypes.byref(d)) == mf.EINVAL
+    assert b"world" in L.mfode_last_global_error()
+    assert L.mfode_parareal_solve(None, 1, 0.0, 0, None) == mf.EINVAL
+    assert L.mfode_dgemm(None, None, None, None, 4, 4, 1.0, 0.0, 0, None) == mf.EINVAL
+
+
+def test_no_oracle_import_in_product_path():
+    """The product path never touches oracle/ (and the oracle never touches the product path)."""
+    pkg = os.path.join(ROOT, "paper_1505_07959_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                code = re.sub(r'"""[\s\S]*?"""|#.*|//.*', "", txt)   # drop docstrings / comments
+                assert "import oracle" not in code and "from oracle" not in code, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith(".py"):
+            code = re.sub(r'"""[\s\S]*?"""|#.*', "", open(os.path.join(ROOT, "oracle", f)).read())
+            assert "paper_1505_07959_b200" not in code and "mfode" not in code, f

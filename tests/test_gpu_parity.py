@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances:
+  * whole solves: relative Frobenius error <= 1e-10 (BASELINE.json north star), in practice ~1e-14;
+  * GEMM: ||C_gpu - C_ref||_F <= 2 n u || |A| |B| ||_F, u = 2^-53 (gamma_n bound applied to both
+    sides);
+  * element-wise stage updates: a few ulp (FMA contraction is the only difference);
+  * bookkeeping (prefix exactness, K = N, logical-rank invariance, A = I): bitwise.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1505_07959_b200 as mf  # noqa: E402
+import workloads  # noqa: E402
+from oracle import dense, spectral  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+U53 = 2.0 ** -53
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback exists)"
+    mf.lib()
+    yield
+
+
+def _dev(a, ld=None):
+    """Host array -> device tensor with leading dimension ld (padding zero), returns the n x n view."""
+    n = a.shape[0]
+    ld = ld or n
+    t = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    t[:, :n] = torch.from_numpy(np.ascontiguousarray(a))
+    return t[:, :n]
+
+
+def relF(x, ref):
+    return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
+# ---------------------------------------------------------------------------------------------
+# kernel level
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("tile", [1, 2, 3])
+@pytest.mark.parametrize("n", [1, 8, 30, 64, 100, 129, 256, 500])
+def test_dgemm_parity(n, tile):
+    rng = np.random.default_rng(n * 10 + tile)
+    A = rng.standard_normal((n, n))
+    B = rng.standard_normal((n, n))
+    ld = n + (n % 2) + (16 if n % 3 == 0 else 0)   # ragged leading dimensions too
+    dA, dB = _dev(A, ld), _dev(B, ld)
+    dD = _dev(np.zeros((n, n)), ld)
+    mf.dgemm(dA, dB, out=dD, tile=tile)
+    D = dD.cpu().numpy()
+    ref = A @ B
+    bound = 2 * n * U53 * np.linalg.norm(np.abs(A) @ np.abs(B))
+    assert np.linalg.norm(D - ref) <= bound
+
+
+@pytest.mark.parametrize("n", [64, 200])
+def test_dgemm_alpha_beta(n):
+    rng = np.random.default_rng(5)
+    A, B, C = (rng.standard_normal((n, n)) for _ in range(3))
+    dD = mf.dgemm(_dev(A), _dev(B), C=_dev(C), alpha=-1.0, beta=1.0)
+    ref = C - A @ B
+    bound = 2 * (n + 1) * U53 * np.linalg.norm(np.abs(A) @ np.abs(B) + np.abs(C))
+    assert np.linalg.norm(dD.cpu().numpy() - ref) <= bound
+
+
+def test_dgemm_large_sampled():
+    """n = 4096 (BASELINE cfg[3]/[4] size, the bench's tile config): sampled rows vs numpy."""
+    n = 4096
+    g = torch.Generator(device="cuda").manual_seed(0)
+    dA = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    dB = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    dD = mf.dgemm(dA, dB)
+    rows = [0, 1, 127, 128, 2047, 4000, 4095]
+    A = dA[rows].cpu().numpy()
+    B = dB.cpu().numpy()
+    ref = A @ B
+    got = dD[rows].cpu().numpy()
+    bound = 2 * n * U53 * np.linalg.norm(np.abs(A) @ np.abs(B))
+    assert np.linalg.norm(got - ref) <= bound
+
+
+@pytest.mark.parametrize("stage", [1, 2, 3, 4])
+@pytest.mark.parametrize("n", [40, 256])
+def test_rk_stage_parity(n, stage):
+    rng = np.random.default_rng(stage)
+    Y, W, X, S = (rng.standard_normal((n, n)) for _ in range(4))
+    h = 1.0 / 64
+    dX, dS, dYn = _dev(X), _dev(S), _dev(np.zeros((n, n)))
+    mf.rk_stage(_dev(Y), _dev(W), dX, dS, dYn, stage, h)
+    K = Y @ W
+    tolK = 2 * n * U53 * np.abs(Y) @ np.abs(W)
+    if stage == 4:
+        refX = X + (h / 6) * (S + K)
+        err = np.abs(dX.cpu().numpy() - refX)
+        assert np.all(err <= (h / 6) * tolK + 4 * U53 * (np.abs(X) + (h / 6) * np.abs(S + K)))
+    else:
+        refS = K if stage == 1 else S + 2 * K
+        c = h if stage == 3 else h / 2
+        refY = X + c * K
+        assert np.all(np.abs(dS.cpu().numpy() - refS) <= 2 * tolK + 4 * U53 * np.abs(refS))
+        assert np.all(np.abs(dYn.cpu().numpy() - refY) <= c * tolK + 4 * U53 * (np.abs(X) + c * np.abs(K)))
+
+
+def test_frobenius_parity():
+    rng = np.random.default_rng(9)
+    X, Y = rng.standard_normal((300, 300)), rng.standard_normal((300, 300))
+    d, x = mf.frobenius(_dev(X), _dev(Y))
+    assert abs(d - np.linalg.norm(X - Y)) <= 1e-13 * d
+    assert abs(x - np.linalg.norm(X)) <= 1e-13 * x
+
+
+# ---------------------------------------------------------------------------------------------
+# solver level
+# ---------------------------------------------------------------------------------------------
+def _solve_gpu(A, flow, T, N, mG, mF, K, tol=0.0, stop=0, world=1, **opts):
+    s = mf.Solver(A, flow, T, N, mG, mF, world=world)
+    for k, v in opts.items():
+        s.set_option(k, v)
+    info = s.solve(K, tol, stop)
+    X = s.result()
+    return s, info, X
+
+
+@pytest.mark.parametrize("n", [3, 40, 100])
+def test_solver_small_vs_oracle(n):
+    w = workloads.random_spd(n, n)
+    N, mG, mF, K = 6, 1, 8, 3
+    s, info, X = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, N, mG, mF, K)
+    ref = dense.solve(w.A, dense.FLOW_INVERSE, 1.0, N, mG, mF, K)
+    assert info["k_done"] == K
+    assert relF(X, ref["X"]) <= 1e-12
+    for k in range(K):
+        assert abs(info["deltas"][k] - ref["deltas"][k]) <= 1e-6 * ref["deltas"][k] + 1e-15
+    s.close()
+
+
+def test_solver_sqrt_small_vs_oracle():
+    m = 5
+    A = workloads.laplacian_2d(m) + np.eye(m * m)
+    N, mG, mF = 64, 2, 32
+    s, info, X = _solve_gpu(A, mf.FLOW_SQRT, 20.0, N, mG, mF, 4, 1e-10, mf.STOP_RESIDUAL)
+    ref = dense.solve(A, dense.FLOW_SQRT, 20.0, N, mG, mF, 4, 1e-10, dense.STOP_RESIDUAL)
+    assert info["k_done"] == ref["k_done"] == 1
+    assert relF(X, ref["X"]) <= 1e-12
+    assert abs(info["residual0"] - ref["residual0"]) <= 1e-6 * ref["residual0"] + 1e-16
+    assert s.residual() <= 1e-10
+
+
+def test_coarse_only_K0():
+    w = workloads.random_spd(24, 1)
+    s, info, X = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, 5, 2, 4, 0)
+    ref = dense.solve(w.A, dense.FLOW_INVERSE, 1.0, 5, 2, 4, 0)
+    assert info["k_done"] == 0
+    assert relF(X, ref["X"]) <= 1e-13
+
+
+def test_prefix_exactness_and_K_equals_N_bitwise():
+    """P5/P6: GPU U^k_n == GPU sequential fine for n <= k, bitwise; K = N exact."""
+    w = workloads.random_spd(48, 2)
+    N = 5
+    s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 6)
+    s.sequential_fine()
+    seq = [s.slice(m) for m in range(N + 1)]
+    for k in range(N + 1):
+        info = s.solve(k)
+        assert info["k_done"] == k
+        for m in range(k + 1):
+            assert np.array_equal(s.slice(m), seq[m]), (k, m)
+    assert np.array_equal(s.result(), seq[N])
+    # and the sequential fine GPU result matches the oracle's sequential fine run
+    ref = dense.solve_sequential_fine(w.A, dense.FLOW_INVERSE, 1.0, N, 6)
+    assert relF(seq[N], ref) <= 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_logical_ranks_bitwise(world):
+    """P9: the slice partition over ranks (contiguous blocks, boundary exchange) changes nothing."""
+    w = workloads.random_spd(64, 3)
+    N = 8
+    _, i1, X1 = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 8, 16, 1e-12, mf.STOP_DELTA)
+    _, iP, XP = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 8, 16, 1e-12, mf.STOP_DELTA, world=world)
+    assert i1["k_done"] == iP["k_done"]
+    assert np.array_equal(X1, XP)
+    assert i1["deltas"] == iP["deltas"]
+
+
+@pytest.mark.parametrize("overlap", [0, 1])
+def test_overlap_and_batch_invariance(overlap):
+    """Speculative overlap and the fine batch size do not change results (bitwise)."""
+    w = workloads.random_spd(80, 4)
+    _, ia, Xa = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, 7, 1, 6, 7, 1e-11, mf.STOP_DELTA, overlap=overlap)
+    _, ib, Xb = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, 7, 1, 6, 7, 1e-11, mf.STOP_DELTA, overlap=1 - overlap,
+                           fine_batch=2, tile=3)
+    assert ia["k_done"] == ib["k_done"]
+    assert np.array_equal(Xa, Xb)
+
+
+def test_identity_exact():
+    """P7: A = I gives exactly I for both flows."""
+    for flow in (mf.FLOW_INVERSE, mf.FLOW_SQRT):
+        _, info, X = _solve_gpu(np.eye(33), flow, 1.0, 4, 1, 3, 3)
+        assert np.array_equal(X, np.eye(33))
+
+
+def test_single_slice():
+    """N = 1 => U^1_1 = F(X0) = the sequential fine solution."""
+    w = workloads.random_spd(20, 6)
+    s, info, X = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, 1, 2, 9, 1)
+    ref = dense.solve_sequential_fine(w.A, dense.FLOW_INVERSE, 1.0, 1, 9)
+    assert relF(X, ref) <= 1e-13
+
+
+def test_nonsymmetric_inverse():
+    """Non-symmetric A: catches a transposed operand anywhere on the GPU path."""
+    n = 50
+    A = workloads.random_nonsymmetric(n, 1)
+    s, info, X = _solve_gpu(A, mf.FLOW_INVERSE, 1.0, 4, 1, 50, 4)
+    ref = dense.solve(A, dense.FLOW_INVERSE, 1.0, 4, 1, 50, 4)
+    assert relF(X, ref["X"]) <= 1e-12
+    assert np.abs(X - np.linalg.inv(A)).max() <= 1e-8 * np.abs(np.linalg.inv(A)).max()
+
+
+def test_nonfinite_reports_bad_slice():
+    """a flow that blows up is reported as ENONFINITE with the first bad slice."""
+    A = np.diag(np.full(16, 40.0))   # q' = (1 - 40) q^2 with coarse Euler h = 1/4: diverges
+    s = mf.Solver(A, mf.FLOW_INVERSE, 1.0, 4, 1, 4)
+    with pytest.raises(mf.MfodeError) as e:
+        s.solve(2, 1e-10, mf.STOP_DELTA)
+    assert e.value.status == mf.ENONFINITE
+
+
+def test_invalid_arguments():
+    with pytest.raises(mf.MfodeError) as e:
+        mf.Solver(np.eye(4), 7, 1.0, 4, 1, 1)
+    assert e.value.status == mf.EINVAL
+    s = mf.Solver(np.eye(4), mf.FLOW_INVERSE, 1.0, 4, 1, 1)
+    with pytest.raises(mf.MfodeError):
+        s.solve(-1)
+    with pytest.raises(mf.MfodeError):
+        s.set_option("nope", 1)
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE.json configs
+# ---------------------------------------------------------------------------------------------
+def test_cfg0_full_vs_dense_oracle():
+    w = workloads.config(0)
+    s, info, X = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    ref = dense.solve(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    assert info["k_done"] == ref["k_done"] == 4
+    assert relF(X, ref["X"]) <= 1e-10
+    assert dense.residual_inverse(w.A, X) < 1e-7          # P3 bound at K = 4
+
+
+def test_cfg1_full_vs_dense_oracle():
+    w = workloads.config(1)
+    s, info, X = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    ref = dense.solve(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    assert info["k_done"] == ref["k_done"]
+    assert relF(X, ref["X"]) <= 1e-10
+    sp = spectral.solve(w.eigvals, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    assert sp["k_done"] == info["k_done"]
+    assert relF(X, spectral.reconstruct(w.eigvecs, sp["X"])) <= 1e-10
+    assert s.residual() < 1e-10
+
+
+@pytest.mark.slow
+def test_cfg2_full_vs_spectral_oracle():
+    w = workloads.config(2)
+    s, info, X = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    sp = spectral.solve(w.eigvals, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    assert info["k_done"] == sp["k_done"]
+    assert relF(X, spectral.reconstruct(w.eigvecs, sp["X"])) <= 1e-10
+
+
+def test_cfg4_full_bench_workload_vs_spectral_oracle():
+    """The bench workload (BASELINE cfg[4], n = 4096, N = 64) in the bench's launch configuration:
+    the full output against the spectral oracle (Kronecker sine basis, exact in exact arithmetic)."""
+    w = workloads.config(4)
+    s, info, X = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    sp = spectral.solve(w.eigvals, w.flow, w.T, w.N, w.m_G, w.m_F, w.K_max, w.tol, w.stop)
+    assert info["k_done"] == sp["k_done"] == 1
+    ref = spectral.reconstruct(w.eigvecs, sp["X"])
+    assert relF(X, ref) <= 1e-10
+    assert info["residual"] <= 1e-10
+    assert abs(info["residual0"] - sp["residual0"]) <= 1e-3 * sp["residual0"] + 1e-15
