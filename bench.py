@@ -240,7 +240,7 @@ def main():
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = e2e_flops / (e2e_ms * 1e-3) / 1e12
+    e2e_value = e2e_flops / (e2e_ms * 1e-3) / 1e12 if args.e2e_steps > 0 else None
     resid = solver.residual()
 
     if rank == 0:
@@ -262,7 +262,7 @@ def main():
             "k_done": infos[-1]["k_done"],
             "residual": resid,
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.e2e_steps,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / max(1, args.e2e_steps),
                     "h2d_bytes_per_step": 8 * w.n * w.n, "d2h_bytes_per_step": 8 * w.n * w.n},
             "gpu_launches": int(sum(i["gpu_launches"] for i in infos)),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
