@@ -145,7 +145,8 @@ MFODE_API int mfode_get_slice(mfode_ctx *h, int n_index, double *U);
 
 /* Tuning knobs (all optional).  key: "fine_batch" (max slices per batched fine launch; 0 = auto),
  * "overlap" (1 = speculative next-iteration fine work overlapped with the correction sweep,
- * 0 = strictly phased), "tile" (0 = auto, 1 = 128x128, 2 = 64x64, 3 = 32x64 GEMM tiles). */
+ * 0 = strictly phased), "tile" (0 = auto, 1 = 128x128, 2 = 64x64, 3 = 32x64 GEMM tiles), "small" (1 = K6
+ * shared-memory persistent kernels, default for n <= 64; 0 = one launch per GEMM). */
 MFODE_API int mfode_set_option(mfode_ctx *h, const char *key, int64_t value);
 
 MFODE_API const char *mfode_last_error(const mfode_ctx *h);

@@ -125,6 +125,7 @@ struct mfode_ctx {
   int* stop_flag = nullptr;  // device
   int cap = 1;               // fine batch capacity (slices per launch)
   int tile = 0;              // 0 auto
+  bool small = false;        // K6 shared-memory kernels (n <= kSmallMaxN)
   bool overlap = true;
   int fine_batch_opt = 0;
   double normA = 0.0;        // ||A||_F
@@ -279,6 +280,12 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
   const int Z = jb - ja;
   const double hF = h->T / ((double)h->N * h->mF);
   const long long me = (long long)mat_elems(h);
+  if (h->small) {
+    const double* M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
+    CUDA_TRY(h, launch_fine_small(h->flow, h->n, h->ld, M, slot(h, R.U[par], ja), slot(h, R.Fk, ja), me, Z, h->mF,
+                                  hF, stop_flag, R.fine));
+    return MFODE_OK;
+  }
   Operand Xu{R.U[par], R.nloc + 1, ja, 1};
   Operand Xf{R.Fk, R.nloc, ja, 1};
   Operand Ya{R.Ya, h->cap, 0, 1}, Yb{R.Yb, h->cap, 0, 1};
@@ -343,7 +350,7 @@ static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
     }
     Rank::ChunkTiming& ct = R.tpool[R.tused++];
     ct.iter = k;
-    ct.launches = h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
+    ct.launches = h->small ? 1 : h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
     ct.flops = (double)(jb - ja) * h->mF * rk4_flops(h);
     CUDA_TRY(h, cudaEventRecord(ct.t0, R.fine));
     TRY(fine_chunk(h, R, par, ja, jb, flag));
@@ -379,8 +386,22 @@ static int recv_boundary(mfode_ctx* h, Rank& R, int par) {
   return MFODE_OK;
 }
 
+static int coarse_small_sweep(mfode_ctx* h, Rank& R, const double* Vin, double* Uslab, int j0, int correct) {
+  const double hG = h->T / ((double)h->N * h->mG);
+  const double* M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
+  CUDA_TRY(h, launch_coarse_small(h->flow, h->n, h->ld, M, Vin, Uslab, R.Gold, R.Fk, (long long)mat_elems(h), j0,
+                                  R.nloc, h->mG, hG, correct, R.coarse));
+  for (int j = j0; j < R.nloc; ++j) CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
+  return MFODE_OK;
+}
+
 static int enqueue_step0(mfode_ctx* h, Rank& R) {
   TRY(recv_boundary(h, R, 0));
+  if (h->small) {
+    TRY(coarse_small_sweep(h, R, R.U[0], R.U[0], 0, 0));
+    TRY(send_boundary(h, R, 0));
+    return MFODE_OK;
+  }
   for (int j = 0; j < R.nloc; ++j) {
     TRY(coarse_G(h, R, R.U[0], R.nloc + 1, j, EPI_EULER, slot(h, R.U[0], j + 1), slot(h, R.Gold, j), nullptr,
                  nullptr));
@@ -395,6 +416,15 @@ static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
   const int cur = k % 2, nxt = (k + 1) % 2;
   const int j0 = std::max(0, k - R.s0);
   if (k < R.s0) TRY(recv_boundary(h, R, nxt));
+  if (h->small) {
+    // the single-CTA sweep needs every F(U^k_n), n >= j0, before it starts
+    for (int j = j0; j < R.nloc; ++j)
+      if (j == j0 || R.chunk_of[j] != R.chunk_of[j - 1]) CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, R.evF[R.chunk_of[j]], 0));
+    const double* Vin = (k >= R.s0) ? slot(h, R.U[cur], j0) : R.U[nxt];
+    TRY(coarse_small_sweep(h, R, Vin, R.U[nxt], j0, 1));
+    TRY(send_boundary(h, R, nxt));
+    return MFODE_OK;
+  }
   for (int j = j0; j < R.nloc; ++j) {
     const double* in_slab;
     int in_idx;
@@ -540,6 +570,7 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   h->mG = mG;
   h->mF = mF;
   h->world = world;
+  h->small = (h->n <= kSmallMaxN);
   int dev = 0;
   if (dist) dev = dist->device;
   else cudaGetDevice(&dev);
@@ -985,6 +1016,11 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
   if (!h || !key) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!strcmp(key, "overlap")) {
     h->overlap = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "small")) {
+    if (value && h->n > kSmallMaxN) return fail(h, MFODE_EINVAL, "small kernels need n <= %d", kSmallMaxN);
+    h->small = value != 0;
     return MFODE_OK;
   }
   if (!strcmp(key, "tile")) {

@@ -35,5 +35,14 @@ long long gemm_tiles(int tile, int n, int num_z);
 void forget_maps(const double* lo, const double* hi);
 
 constexpr int kFrobPartials = 2 * 296;
+constexpr int kSmallMaxN = 64;   // K6 small-n persistent kernels handle n <= 64
+
+// K6: all m_F RK4 steps of Z slices (one CTA each) in shared memory; M = B (inverse) or A (sqrt)
+cudaError_t launch_fine_small(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
+                              long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st);
+// K6: the rank's sequential coarse sweep (Step 0 if correct == 0, else the correction) in one CTA
+cudaError_t launch_coarse_small(int flow, int n, int ld, const double* M, const double* Vin, double* U, double* Gold,
+                                const double* Fk, long long mstride, int j0, int nloc, int mG, double h, int correct,
+                                cudaStream_t st);
 
 }  // namespace mfode

@@ -16,6 +16,7 @@
 
 #include "gemm.cuh"
 #include "internal.h"
+#include "small.cuh"
 
 namespace mfode {
 
@@ -331,6 +332,50 @@ cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, G
     case EPI_RESID: return dispatch_tile<EPI_RESID>(tile, ma, mb, p, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// --------------------------------------------------------------------------------------------
+// K6 small-n launchers
+// --------------------------------------------------------------------------------------------
+template <int NP>
+static cudaError_t fine_small_np(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
+                                 long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st) {
+  const size_t smem = 5 * SmallCfg<NP>::MAT * sizeof(double);
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(fine_smem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  fine_smem_kernel<NP><<<Z, kSmallThreads, smem, st>>>(flow, n, ld, M, Uin, Fout, mstride, mF, h, flag);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <int NP>
+static cudaError_t coarse_small_np(int flow, int n, int ld, const double* M, const double* Vin, double* U,
+                                   double* Gold, const double* Fk, long long mstride, int j0, int nloc, int mG,
+                                   double h, int correct, cudaStream_t st) {
+  const size_t smem = 4 * SmallCfg<NP>::MAT * sizeof(double);
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(coarse_smem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  coarse_smem_kernel<NP><<<1, kSmallThreads, smem, st>>>(flow, n, ld, M, Vin, U, Gold, Fk, mstride, j0, nloc, mG, h,
+                                                          correct);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fine_small(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
+                              long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st) {
+  if (n <= 32) return fine_small_np<32>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+  return fine_small_np<64>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+}
+
+cudaError_t launch_coarse_small(int flow, int n, int ld, const double* M, const double* Vin, double* U, double* Gold,
+                                const double* Fk, long long mstride, int j0, int nloc, int mG, double h, int correct,
+                                cudaStream_t st) {
+  if (n <= 32) return coarse_small_np<32>(flow, n, ld, M, Vin, U, Gold, Fk, mstride, j0, nloc, mG, h, correct, st);
+  return coarse_small_np<64>(flow, n, ld, M, Vin, U, Gold, Fk, mstride, j0, nloc, mG, h, correct, st);
 }
 
 }  // namespace mfode

@@ -292,3 +292,37 @@ def test_cfg4_full_bench_workload_vs_spectral_oracle():
     assert relF(X, ref) <= 1e-10
     assert info["residual"] <= 1e-10
     assert abs(info["residual0"] - sp["residual0"]) <= 1e-3 * sp["residual0"] + 1e-15
+
+
+@pytest.mark.parametrize("n", [5, 32, 48, 64])
+@pytest.mark.parametrize("flow", [0, 1])
+def test_small_kernels_bitwise_equal_gemm_path(n, flow):
+    """K6 (whole propagation in one CTA's shared memory) uses the DMMA issue order, lane->k mapping
+    and epilogue arithmetic of the launch-per-GEMM path, so the two agree bitwise; both match the oracle."""
+    if flow == 0:
+        w = workloads.random_spd(n, 10 + n)
+        A, T, N, mG, mF = w.A, 1.0, 8, 1, 16
+    else:
+        m = int(round(math.sqrt(n)))
+        A = workloads.laplacian_2d(m) + np.eye(m * m) if m * m == n else workloads.random_spd(n, 3).A + np.eye(n)
+        T, N, mG, mF = 20.0, 64, 2, 32
+    res = []
+    for small in (1, 0):
+        _, info, X = _solve_gpu(A, flow, T, N, mG, mF, 3, small=small)
+        res.append((info, X))
+    assert np.array_equal(res[0][1], res[1][1])
+    assert res[0][0]["deltas"] == res[1][0]["deltas"]
+    ref = dense.solve(A, flow, T, N, mG, mF, 3)
+    assert relF(res[0][1], ref["X"]) <= 1e-12
+    assert res[0][0]["gpu_launches"] < res[1][0]["gpu_launches"]
+
+
+def test_small_kernels_logical_ranks_and_sequential():
+    w = workloads.config(0)
+    s1, i1, X1 = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 8, 1e-13, mf.STOP_DELTA)
+    s4, i4, X4 = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 8, 1e-13, mf.STOP_DELTA, world=4)
+    assert np.array_equal(X1, X4) and i1["k_done"] == i4["k_done"]
+    s1.solve(w.N)
+    XN = s1.result()
+    s1.sequential_fine()
+    assert np.array_equal(s1.result(), XN)     # P5 on the K6 path

@@ -1,0 +1,117 @@
+"""World-size-2 (and 3) CPU tests of the multi-rank schedule over torch.distributed 'gloo'.
+
+The CUDA driver (paper_1505_07959_b200/csrc/driver.cu) partitions the N time slices into
+contiguous blocks (mfode_partition, the library's host-only function used here too), keeps U
+ping-pong buffered by sweep parity, skips slices n < k in sweep k, and moves the boundary state
+rank g -> g+1 after Step 0 and after each correction sweep, and broadcasts the stop metric from
+the last rank.  This test runs exactly that schedule with the CPU oracle's propagators in one
+process per rank, exchanging boundary states with gloo send/recv, and checks the result is
+bitwise identical to the single-process oracle (P9: results do not depend on the rank count).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_1505_07959_b200 as mf
+import workloads
+from oracle import dense
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, A, cfg, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    T, N, mG, mF, K_max, tol, stop = cfg
+    n = A.shape[0]
+    s0, nloc = mf.partition(N, world, rank)
+    s1 = s0 + nloc
+    rhs = dense.make_rhs(A, dense.FLOW_INVERSE)
+    hG, hF = T / (N * mG), T / (N * mF)
+    G = lambda x: dense.euler(rhs, x, hG, mG)
+    F = lambda x: dense.rk4(rhs, x, hF, mF)
+    I = np.eye(n)
+    U = [[None] * (nloc + 1), [None] * (nloc + 1)]
+    Fk = [None] * nloc
+    Gold = [None] * nloc
+
+    def send(x):
+        if rank < world - 1:
+            dist.send(torch.from_numpy(np.ascontiguousarray(x)), dst=rank + 1)
+
+    def recv():
+        t = torch.empty((n, n), dtype=torch.float64)
+        dist.recv(t, src=rank - 1)
+        return t.numpy()
+
+    # Step 0
+    U[0][0] = I if rank == 0 else recv()
+    if rank == 0:
+        U[1][0] = I
+    for j in range(nloc):
+        g = G(U[0][j])
+        U[0][j + 1] = g
+        Gold[j] = g
+    send(U[0][nloc])
+    k_done = 0
+    K_eff = min(K_max, N)
+    for k in range(K_eff):
+        cur, nxt = k % 2, (k + 1) % 2
+        # fine (active slices n >= k)
+        if k < s1:
+            for j in range(max(0, k - s0), nloc):
+                Fk[j] = F(U[cur][j])
+        # correction
+        if k < s1:
+            j0 = max(0, k - s0)
+            if k < s0:
+                U[nxt][0] = recv()
+            for j in range(j0, nloc):
+                v = U[cur][j0] if (j == j0 and k >= s0) else U[nxt][j]
+                g = G(v)
+                U[nxt][j + 1] = Fk[j] + (g - Gold[j])
+                Gold[j] = g
+            send(U[nxt][nloc])
+        # stop metric from the last rank
+        m = torch.zeros(1, dtype=torch.float64)
+        if rank == world - 1:
+            m[0] = dense.frob(U[nxt][nloc] - U[cur][nloc]) / dense.frob(U[nxt][nloc])
+        dist.broadcast(m, src=world - 1)
+        k_done = k + 1
+        if stop == dense.STOP_DELTA and m.item() <= tol:
+            break
+    if rank == world - 1:
+        q.put((k_done, U[k_done % 2][nloc]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_schedule_bitwise(world):
+    w = workloads.random_spd(12, 7)
+    cfg = (1.0, 7, 1, 5, 7, 1e-12, dense.STOP_DELTA)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, w.A, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    k_done, X = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = dense.solve(w.A, dense.FLOW_INVERSE, *cfg[:5], tol=cfg[5], stop=cfg[6])
+    assert k_done == ref["k_done"]
+    assert np.array_equal(X, ref["X"])
