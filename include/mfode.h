@@ -63,7 +63,8 @@ typedef enum {
 
 typedef enum {
   MFODE_FLOW_INVERSE = 0, /* F(X) = X (I - A) X, X0 = I  => X(1) = A^{-1} */
-  MFODE_FLOW_SQRT = 1     /* F(X) = A - X^2,     X0 = I  => X(inf) = A^{1/2}         */
+  MFODE_FLOW_SQRT = 1,    /* F(X) = A - X^2,     X0 = I  => X(inf) = A^{1/2}         */
+  MFODE_FLOW_EXP = 2      /* F(X) = A X,         X0 = I  => X(1) = exp(A)       (Ex. 2) */
 } mfode_flow;
 
 typedef enum {
@@ -129,7 +130,8 @@ MFODE_API int mfode_parareal_solve(mfode_ctx *h, int K_max, double tol, int stop
 MFODE_API int mfode_sequential_fine(mfode_ctx *h, mfode_solve_info *info);
 
 /* Residual of the current result X = U_N: inverse flow ||A X - I||_F / sqrt(n);
- * sqrt flow ||A - X^2||_F / ||A||_F.  One GEMM with a fused deterministic reduction. */
+ * sqrt flow ||A - X^2||_F / ||A||_F.  One GEMM with a fused deterministic reduction.
+ * The exp flow has no residual of this kind: EINVAL (and MFODE_STOP_RESIDUAL is rejected for it). */
 MFODE_API int mfode_residual(mfode_ctx *h, double *rel_residual);
 
 /* Copy the current result X = U_N to HOST memory (row-major n*n, caller-owned).  In NCCL mode the

@@ -8,6 +8,7 @@ Citations (P:n = PAPER.md line n):
   * inverse flow F(X) = X (I - A) X, X(0) = I, X(1) = A^{-1}             P:44 (§1); eq. (eqQ)
   * steady-state flow dX/dt = F(X), F(X*) = 0 <=> X* = f(A)              P:46-51 eq. (stat)
     (instance F(X) = A - X^2, X* = A^{1/2}: BASELINE.json north star)
+  * exponential flow dQ/dt = A Q, Q(0) = I, Q(1) = exp(A)                 Example 2
   * coarse propagator G = forward Euler                                   P:129, P:182 ("Euler explicit")
   * fine propagator F = Runge-Kutta ("Runge Kutta method can be applied") P:44; classical RK4 (R1)
   * Algorithm 1, Step 0 U^0_{n+1} = G(U^0_n), U^0_0 = u0                 P:136-139 eq. (eqStep0)
@@ -31,6 +32,7 @@ import numpy as np
 
 FLOW_INVERSE = 0
 FLOW_SQRT = 1
+FLOW_EXP = 2
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
@@ -49,12 +51,19 @@ def rhs_sqrt(A: np.ndarray) -> Callable:
     return lambda X: A - X @ X
 
 
+def rhs_exp(A: np.ndarray) -> Callable:
+    """F(X) = A X, X(0) = I  =>  X(1) = exp(A) (Example 2, eq. eqQ)."""
+    return lambda X: A @ X
+
+
 def make_rhs(A: np.ndarray, flow: int) -> Callable:
     if flow == FLOW_INVERSE:
         B = np.eye(A.shape[0]) - A          # formed once (R2)
         return rhs_inverse(B)
     if flow == FLOW_SQRT:
         return rhs_sqrt(A)
+    if flow == FLOW_EXP:
+        return rhs_exp(A)
     raise ValueError(f"unknown flow {flow}")
 
 
@@ -181,10 +190,12 @@ def residual_sqrt(A: np.ndarray, X: np.ndarray) -> float:
     return frob(A - X @ X) / frob(A)
 
 
-def flow_residual(A: np.ndarray, flow: int) -> Callable:
+def flow_residual(A: np.ndarray, flow: int) -> Optional[Callable]:
     if flow == FLOW_INVERSE:
         return lambda X: residual_inverse(A, X)
-    return lambda X: residual_sqrt(A, X)
+    if flow == FLOW_SQRT:
+        return lambda X: residual_sqrt(A, X)
+    return None     # the exp flow has no residual of this kind
 
 
 def solve(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,

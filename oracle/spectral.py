@@ -7,6 +7,7 @@ with scalar coefficients, so for A = V diag(lam) V^T every iterate is U^k_n = V 
 where u^k_n is the SAME algorithm applied to the scalar ODE
     inverse: q' = q ((1 - lam) q)        (the eigen-image of X (I - A) X)
     sqrt:    x' = lam - x^2              (the eigen-image of A - X^2)
+    exp:     x' = lam x                  (the eigen-image of A X, Example 2 P:193-201)
 with x0 = 1.  This is the paper's own diagonalisation argument.  Frobenius norms of
 V diag(u) V^T are 2-norms of u (V orthogonal), so the delta/residual stop tests carry over.
 The state of the generic dense.parareal is then a length-n vector of scalars (elementwise ops).
@@ -29,6 +30,8 @@ def scalar_rhs(lam, flow: int):
         return lambda q: q * (b * q)
     if flow == dense.FLOW_SQRT:
         return lambda x: lam - x * x
+    if flow == dense.FLOW_EXP:
+        return lambda x: lam * x
     raise ValueError(flow)
 
 
@@ -43,6 +46,8 @@ def solve(eigvals: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, 
     if flow == dense.FLOW_INVERSE:
         # ||A X - I||_F / sqrt(n) = ||lam u - 1||_2 / sqrt(n)
         residual = lambda u: norm(lam * u - 1.0) / math.sqrt(lam.size)
+    elif flow == dense.FLOW_EXP:
+        residual = None
     else:
         # ||A - X^2||_F / ||A||_F = ||lam - u^2||_2 / ||lam||_2
         residual = lambda u: norm(lam - u * u) / norm(lam)

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(HERE, "libmfode.so")
 
 FLOW_INVERSE = 0
 FLOW_SQRT = 1
+FLOW_EXP = 2
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
@@ -277,4 +278,4 @@ def version() -> str:
 
 def rk4_flops_per_step(n: int, flow: int) -> float:
     """Algorithmic flops of one RK4 step: 4 stages x (2 GEMMs inverse | 1 GEMM sqrt) x 2n^3."""
-    return (16.0 if flow == FLOW_INVERSE else 8.0) * float(n) ** 3
+    return (16.0 if flow == FLOW_INVERSE else 8.0) * float(n) ** 3   # exp: 4 stages x 1 GEMM

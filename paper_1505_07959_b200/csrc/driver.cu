@@ -212,6 +212,7 @@ static GemmParams base_params(const mfode_ctx* h, int num_z) {
 // rhs GEMM(s) of the flow for batch z: returns via epilogue params; Y operand given as Operand.
 // inverse: W = B Y (EPI_STORE into Wbuf), then K = Y W with epilogue `epi`
 // sqrt:    K = -(Y Y) + A with epilogue `epi`
+// exp:     K = A Y with epilogue `epi`
 static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, int num_z, GemmParams p, int epi,
                       cudaStream_t st, cudaEvent_t wait_before_second) {
   const long long me = (long long)mat_elems(h);
@@ -226,12 +227,18 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     p.alpha = 1.0;
     p.beta = 0.0;
     CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Wop, p, st));
-  } else {
+  } else if (h->flow == MFODE_FLOW_SQRT) {
     if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
     p.alpha = -1.0;
     p.beta = 1.0;
     p.C = MatRef{h->A, 0};
     CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Y, p, st));
+  } else {   // MFODE_FLOW_EXP: K = A Y
+    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    Operand Aop{h->A, 1, 0, 0};
+    CUDA_TRY(h, launch_gemm(epi, h->tile, Aop, Y, p, st));
   }
   return MFODE_OK;
 }
@@ -320,13 +327,42 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
   return MFODE_OK;
 }
 
+// Slices per batched fine launch: balanced chunks whose total number of persistent-CTA tile
+// rounds (tiles / concurrently resident CTAs, rounded up per launch) is minimal -- the last,
+// partial round of every launch is idle tensor time.  Ties go to larger chunks (fewer launches).
+static int fine_chunk_size(const mfode_ctx* h, int active) {
+  if (h->small || active <= 1) return std::max(1, std::min(active, h->cap));
+  const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, std::min(active, h->cap));
+  const long long t1 = gemm_tiles(tile, h->n, 1);
+  const long long slots = 148LL * (tile == TILE_128 ? 1 : (tile == TILE_64 ? 2 : 4));
+  const long long launches = (long long)h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
+  const long long euler_gemms = (long long)h->mG * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
+  const long long coarse_rounds = (t1 + slots - 1) / slots;
+  int best = 1;
+  long long best_cost = -1;
+  for (int s = std::min(active, h->cap); s >= 1; --s) {
+    const int nch = (active + s - 1) / s;
+    const int q = active / nch, r = active % nch;   // r chunks of q+1, nch-r of q
+    // fine tile rounds (every launch's last round is partly idle) + the correction steps of the
+    // last chunk, which can only run after the whole fine sweep (the sweep's tail)
+    const long long cost =
+        launches * (r * ((t1 * (q + 1) + slots - 1) / slots) + (nch - r) * ((t1 * q + slots - 1) / slots)) +
+        (long long)(r == nch ? q + 1 : q) * euler_gemms * coarse_rounds;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = (active + nch - 1) / nch;
+    }
+  }
+  return best;
+}
+
 static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
   if (k >= R.s1) return MFODE_OK;
   const int ja0 = std::max(0, k - R.s0);
   const int active = R.nloc - ja0;
   if (active <= 0) return MFODE_OK;
-  const int nchunks = (active + h->cap - 1) / h->cap;
-  const int size = (active + nchunks - 1) / nchunks;
+  const int size = fine_chunk_size(h, active);
+  const int nchunks = (active + size - 1) / size;
   if ((int)R.evF.size() < nchunks) {
     int old = (int)R.evF.size();
     R.evF.resize(nchunks);
@@ -556,7 +592,8 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   *out = nullptr;
   if (!A) return set_global_err(MFODE_EINVAL, "A is NULL");
   if (n < 1 || n > 65536) return set_global_err(MFODE_EINVAL, "n=%lld out of range [1, 65536]", (long long)n);
-  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT) return set_global_err(MFODE_EINVAL, "unknown flow %d", flow);
+  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT && flow != MFODE_FLOW_EXP)
+    return set_global_err(MFODE_EINVAL, "unknown flow %d", flow);
   if (!(T > 0.0) || !std::isfinite(T)) return set_global_err(MFODE_EINVAL, "T must be finite and > 0");
   if (N < 1 || mG < 1 || mF < 1) return set_global_err(MFODE_EINVAL, "N, coarse_steps, fine_steps must be >= 1");
   int world = dist ? dist->world : 1;
@@ -588,11 +625,12 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   }
   // fine batch capacity: enough batched tiles to fill the chip, bounded by the slice count
   {
+    // Scratch for up to `cap` in-flight slices (3-4 matrices each) within a 16 GiB budget; the
+    // chunk size actually used per sweep is chosen by fine_chunk_size() to minimise tile rounds.
     const int nloc_max = (N + world - 1) / world;
-    const int t128 = (int)gemm_tiles(TILE_128, h->n, 1);
-    int cap = std::max(1, (int)((8LL * 148 + t128 - 1) / t128));
-    if (h->n <= 512) cap = nloc_max;   // small matrices: batch every slice of the rank
-    h->cap = std::min(cap, nloc_max);
+    const double per_slice = 4.0 * 8.0 * (double)h->n * (double)h->ld;
+    const int budget = (int)std::max(1.0, std::floor(16.0 * (1LL << 30) / per_slice));
+    h->cap = std::max(1, std::min(nloc_max, budget));
   }
   // ranks
   const int nranks_here = h->nccl_mode ? 1 : world;
@@ -684,6 +722,8 @@ static int first_bad_slice(mfode_ctx* h) {
 
 static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
   if (K_max < 0 || !(tol >= 0.0) || stop < 0 || stop > 2) return fail(h, MFODE_EINVAL, "bad K_max/tol/stop");
+  if (stop == MFODE_STOP_RESIDUAL && h->flow == MFODE_FLOW_EXP)
+    return fail(h, MFODE_EINVAL, "the exp flow has no residual stop test");
   CUDA_TRY(h, cudaSetDevice(h->device));
   const long long L0 = g_launches.load();
   const int K_eff = std::min(K_max, h->N);
@@ -950,6 +990,7 @@ int mfode_sequential_fine(mfode_ctx* h, mfode_solve_info* info) {
 int mfode_residual(mfode_ctx* h, double* rel) {
   if (!h || !rel) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!h->has_result) return fail(h, MFODE_EINVAL, "no result yet (call a solve first)");
+  if (h->flow == MFODE_FLOW_EXP) return fail(h, MFODE_EINVAL, "the exp flow has no residual");
   CUDA_TRY(h, cudaSetDevice(h->device));
   Rank& L = last_rank(h);
   if (owns_last(h)) {
@@ -1016,6 +1057,10 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
   if (!h || !key) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!strcmp(key, "overlap")) {
     h->overlap = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "pdl")) {   // process-wide: programmatic dependent launch of the GEMMs
+    g_pdl = value != 0;
     return MFODE_OK;
   }
   if (!strcmp(key, "small")) {

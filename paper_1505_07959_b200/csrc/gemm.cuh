@@ -92,8 +92,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmParams p) {
   using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>;
-  if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
-
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -119,6 +117,11 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     fence_proxy_async();
   }
   __syncthreads();
+  // PDL: let the next kernel of the stream start its prologue while this grid runs, then wait for
+  // the previous grid (all of its writes visible) before touching global memory.
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
 
   if constexpr (Cfg::kSetMaxNReg) {
     if (warp >= Cfg::kConsumerWarps)
@@ -178,8 +181,9 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
 #pragma unroll
       for (int j = 0; j < 2 * Cfg::NG; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    bool ready = false;   // full[stage] already observed complete by the early probe
     for (int kt = 0; kt < KT; ++kt) {
-      mbar_wait(&full[stage], phase);
+      if (!ready) mbar_wait(&full[stage], phase);
       const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
       const uint32_t sB = sA + Cfg::kABytes;
 #pragma unroll
@@ -200,6 +204,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
             bf[ng][s] = lds128(sB + grp * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
           }
         }
+        if (kb == 1) {
+          // Every shared-memory read of this stage is issued: release it to the producer now
+          // (the arrive has release semantics), and probe the next stage's full barrier so the
+          // probe's latency hides behind this k-step's DMMAs instead of stalling the next one.
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          const int ns = (stage + 1 == STAGES) ? 0 : stage + 1;
+          ready = (kt + 1 < KT) && mbar_test_wait(&full[ns], ns == 0 ? (phase ^ 1) : phase);
+        }
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
@@ -212,8 +225,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
             }
           }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
 

@@ -20,6 +20,7 @@ struct Operand {
 };
 
 extern std::atomic<long long> g_launches;
+extern bool g_pdl;   // programmatic dependent launch for the GEMM kernels (option "pdl")
 
 cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st);
 cudaError_t launch_i_minus(double* B, const double* A, int n, int ld, cudaStream_t st);

@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <algorithm>
 
 #include "gemm.cuh"
 #include "internal.h"
@@ -21,6 +22,7 @@
 namespace mfode {
 
 std::atomic<long long> g_launches{0};
+bool g_pdl = true;
 
 // --------------------------------------------------------------------------------------------
 // Element-wise kernels (HBM-bound; 16-byte vector accesses; padding columns kept at zero)
@@ -283,11 +285,29 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
     occ = o > 0 ? o : 1;
   });
   const long long tiles = (long long)((p.n + BM - 1) / BM) * ((p.n + BN - 1) / BN) * p.num_z;
+  // Bounded persistence: a CTA owns at most ~2 ms of tiles.  Kernels are never preempted, so a grid
+  // that pinned every SM for a whole (batched, ~100 ms) launch would starve the high-priority coarse
+  // stream (the sequential critical path); retiring CTAs every ~2 ms lets its CTAs in.
+  const double tile_s = 2.0 * BM * BN * (double)p.n / (37e12 / (num_sms() * occ));
+  const long long max_tiles_per_cta = std::max<long long>(1, (long long)(2e-3 / tile_s));
   long long grid = (long long)num_sms() * occ;
+  grid = std::max(grid, (tiles + max_tiles_per_cta - 1) / max_tiles_per_cta);
   if (grid > tiles) grid = tiles;
-  kern<<<(unsigned)grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(ma, mb, p);
+  // Programmatic dependent launch: this grid may be scheduled while the previous kernel of the
+  // stream drains; the kernel's griddepcontrol.wait orders every global access after it.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
   ++g_launches;
-  return cudaGetLastError();
+  return e;
 }
 
 int tile_box_rows(int tile) { return tile == TILE_128 ? 128 : (tile == TILE_64 ? 64 : 32); }

@@ -82,7 +82,8 @@ __device__ __forceinline__ void store_mat(double* __restrict__ dst, const double
   }
 }
 
-// K = F(Y) in registers.  inverse: W = B Y (to smem W), K = Y W;  sqrt: K = -(Y Y) + A (A in `M`).
+// K = F(Y) in registers.  inverse: W = B Y (to smem W), K = Y W;  sqrt: K = -(Y Y) + A (A in `M`);
+// exp: K = A Y.
 template <int NP>
 __device__ __forceinline__ void rhs_regs(int flow, const double* M, const double* Y, double* W,
                                          double (&K)[SmallCfg<NP>::TPW][2]) {
@@ -100,6 +101,8 @@ __device__ __forceinline__ void rhs_regs(int flow, const double* M, const double
       }
     __syncthreads();
     smem_gemm<NP>(Y, W, K);
+  } else if (flow == 2) {   // exp: K = A Y
+    smem_gemm<NP>(M, Y, K);
   } else {
     smem_gemm<NP>(Y, Y, K);
 #pragma unroll

@@ -317,6 +317,22 @@ def test_small_kernels_bitwise_equal_gemm_path(n, flow):
     assert res[0][0]["gpu_launches"] < res[1][0]["gpu_launches"]
 
 
+@pytest.mark.parametrize("n", [40, 200])
+def test_exp_flow_vs_oracle(n):
+    """§8(f) f1: exp flow (Example 2) on the same kernels: GPU vs oracle and vs expm."""
+    import scipy.linalg
+    A = workloads.random_nonsymmetric(n, 5, scale=1.0) - np.eye(n)
+    N, mG, mF, K = 8, 2, 16, 8
+    s, info, X = _solve_gpu(A, mf.FLOW_EXP, 1.0, N, mG, mF, K, 1e-13, mf.STOP_DELTA)
+    ref = dense.solve(A, dense.FLOW_EXP, 1.0, N, mG, mF, K, 1e-13, dense.STOP_DELTA)
+    assert info["k_done"] == ref["k_done"]
+    assert relF(X, ref["X"]) <= 1e-12
+    E = scipy.linalg.expm(A)
+    assert relF(X, E) <= 1e-8
+    with pytest.raises(mf.MfodeError):
+        s.residual()
+
+
 def test_small_kernels_logical_ranks_and_sequential():
     w = workloads.config(0)
     s1, i1, X1 = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 8, 1e-13, mf.STOP_DELTA)

@@ -274,6 +274,25 @@ def test_diagonal_closed_form_cfg_spectra():
         np.testing.assert_allclose(s["X"], 1.0 / lam, rtol=1e-12)
 
 
+def test_exp_flow_against_expm():
+    """Example 2: dQ/dt = A Q, Q(0) = I => Q(1) = exp(A).  The sequential fine RK4
+    solution matches scipy's expm (the library definition) within the RK4 error, for a
+    non-symmetric A; and parareal at K = N equals it bitwise (P5)."""
+    import scipy.linalg
+    n = 10
+    A = workloads.random_nonsymmetric(n, 3, scale=1.0) - np.eye(n)
+    N, mF = 5, 40
+    rhs = dense.make_rhs(A, dense.FLOW_EXP)
+    S = dense.sequential_fine(rhs, np.eye(n), 1.0, N, mF)
+    E = scipy.linalg.expm(A)
+    assert np.abs(S[N] - E).max() <= 1e-9 * np.abs(E).max()
+    out = dense.solve(A, dense.FLOW_EXP, 1.0, N, 1, mF, N)
+    assert np.array_equal(out["X"], S[N])
+    # exp(A) exp(-A) = I
+    Sm = dense.sequential_fine(dense.make_rhs(-A, dense.FLOW_EXP), np.eye(n), 1.0, N, mF)
+    assert np.abs(S[N] @ Sm[N] - np.eye(n)).max() < 1e-9
+
+
 def test_config_workloads_shapes():
     """workloads builds what BASELINE.json names (sizes, symmetry, spectra)."""
     for i in (0, 1, 2):

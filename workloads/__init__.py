@@ -21,6 +21,7 @@ import numpy as np
 
 FLOW_INVERSE = 0   # F(X) = X (I - A) X, X0 = I, T = 1   => X(1) = A^{-1}    (eq. eqQ)
 FLOW_SQRT = 1      # F(X) = A - X^2,     X0 = I, T large => X* = A^{1/2}   (north star)
+FLOW_EXP = 2       # F(X) = A X,         X0 = I, T = 1   => X(1) = exp(A)   (Example 2)
 
 STOP_FIXED_K = 0   # run exactly K_max correction sweeps
 STOP_DELTA = 1     # ||U_N^{k+1} - U_N^k||_F / ||U_N^{k+1}||_F <= tol   (BJ cfg[1]; reading R6)
