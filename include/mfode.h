@@ -64,7 +64,10 @@ typedef enum {
 typedef enum {
   MFODE_FLOW_INVERSE = 0, /* F(X) = X (I - A) X, X0 = I  => X(1) = A^{-1} */
   MFODE_FLOW_SQRT = 1,    /* F(X) = A - X^2,     X0 = I  => X(inf) = A^{1/2}         */
-  MFODE_FLOW_EXP = 2      /* F(X) = A X,         X0 = I  => X(1) = exp(A)       (Ex. 2) */
+  MFODE_FLOW_EXP = 2,     /* F(X) = A X,         X0 = I  => X(1) = exp(A)       (Ex. 2) */
+  MFODE_FLOW_TRIG = 3     /* U = (X, Y), X' = A Y, Y' = -A X, U(0) = (0, I) => U(1) = (sin A, cos A)
+                             (Ex. 3, eq. eqB P:441-456 with X0 = 0).  The state is the 2n x n stack
+                             [X; Y]: results and slices are 2n x n (row-major, sin block first). */
 } mfode_flow;
 
 typedef enum {
@@ -153,6 +156,27 @@ MFODE_API int mfode_set_option(mfode_ctx *h, const char *key, int64_t value);
 
 MFODE_API const char *mfode_last_error(const mfode_ctx *h);
 MFODE_API void mfode_destroy(mfode_ctx *h);
+
+/* Algorithm 5: cos(A) for a HOST matrix A (row-major n*n, copied).  m = the smallest
+ * m >= 0 with 2^-m ||A||_inf <= 1, A0 = 2^-m A; C0 = cos(A0) by classical parareal on the trig
+ * block flow (MFODE_FLOW_TRIG, T = 1, N_slices / coarse / fine steps as in mfode_create, K_max /
+ * tol / stop as in mfode_parareal_solve); then C_{i+1} = 2 C_i^2 - I, m times, on the GPU.
+ * C: HOST n*n output (caller-owned); *m_out (nullable) receives m; info (nullable) the solve's
+ * info.  dist as in mfode_create (collective in NCCL mode).  Returns as mfode_parareal_solve. */
+MFODE_API int mfode_cosine(const double *A, int64_t n, int N_slices, int coarse_steps, int fine_steps, int K_max,
+                           double tol, int stop, const mfode_dist *dist, double *C, int *m_out,
+                           mfode_solve_info *info);
+
+/* Algorithm 8 (Example 5): accelerated steady-state inverse, dX/dt = I - A X,
+ *   X^{k+1} = X^k + dt (I - A X^k + u^k),  u^{k+1} = (I - dt A) u^k,  u^0 = E0 (~ A^{-1} - X^0).
+ * A, X0 (NULL -> 0), E0 (NULL -> 0: the unaccelerated flow) are HOST row-major n*n (copied).
+ * Runs at most max_steps steps; with tol > 0 stops at the first checked step (every check_every
+ * steps) with ||A X - I||_F / sqrt(n) <= tol.  X: HOST n*n output; *steps_done and *residual
+ * (nullable) receive the step count and the final residual.  Sequential in k, one GPU.
+ * Returns OK, NOT_CONVERGED (tol > 0 not met), ENONFINITE, EINVAL, ECUDA. */
+MFODE_API int mfode_accel_inverse(const double *A, const double *X0, const double *E0, int64_t n, double dt,
+                                  int max_steps, double tol, int check_every, double *X, int *steps_done,
+                                  double *residual);
 
 /* ---- kernel-level entry points (parity tests, roofline measurement) ---------------------- */
 

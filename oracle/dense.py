@@ -33,6 +33,7 @@ import numpy as np
 FLOW_INVERSE = 0
 FLOW_SQRT = 1
 FLOW_EXP = 2
+FLOW_TRIG = 3
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
@@ -56,6 +57,20 @@ def rhs_exp(A: np.ndarray) -> Callable:
     return lambda X: A @ X
 
 
+def rhs_trig(A: np.ndarray) -> Callable:
+    """Example 3, eq. (eqB) with X0 = 0: U = (X; Y) stacked 2n x n,
+    dX/dt = A Y, dY/dt = -A X, U(0) = (0; I)  =>  U(1) = (sin A; cos A)."""
+    n = A.shape[0]
+    return lambda U: np.vstack([A @ U[n:], -(A @ U[:n])])
+
+
+def initial_state(n: int, flow: int) -> np.ndarray:
+    """X0 = I; the trig block flow starts at (sin 0; cos 0) = (0; I)."""
+    if flow == FLOW_TRIG:
+        return np.vstack([np.zeros((n, n)), np.eye(n)])
+    return np.eye(n)
+
+
 def make_rhs(A: np.ndarray, flow: int) -> Callable:
     if flow == FLOW_INVERSE:
         B = np.eye(A.shape[0]) - A          # formed once (R2)
@@ -64,6 +79,8 @@ def make_rhs(A: np.ndarray, flow: int) -> Callable:
         return rhs_sqrt(A)
     if flow == FLOW_EXP:
         return rhs_exp(A)
+    if flow == FLOW_TRIG:
+        return rhs_trig(A)
     raise ValueError(f"unknown flow {flow}")
 
 
@@ -195,7 +212,7 @@ def flow_residual(A: np.ndarray, flow: int) -> Optional[Callable]:
         return lambda X: residual_inverse(A, X)
     if flow == FLOW_SQRT:
         return lambda X: residual_sqrt(A, X)
-    return None     # the exp flow has no residual of this kind
+    return None     # the exp and trig flows have no residual of this kind
 
 
 def solve(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,
@@ -204,7 +221,7 @@ def solve(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max:
     """f(A) by parareal on the flow's ODE with X0 = I."""
     A = np.asarray(A, dtype=np.float64)
     rhs = make_rhs(A, flow)
-    X0 = np.eye(A.shape[0])
+    X0 = initial_state(A.shape[0], flow)
     # the residual is recorded for every flow; it drives the stop only for STOP_RESIDUAL
     return parareal(rhs, X0, T, N, m_G, m_F, K_max, tol, stop, frob, flow_residual(A, flow),
                     skip_prefix, keep_history)
@@ -212,4 +229,43 @@ def solve(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max:
 
 def solve_sequential_fine(A: np.ndarray, flow: int, T: float, N: int, m_F: int) -> np.ndarray:
     A = np.asarray(A, dtype=np.float64)
-    return sequential_fine(make_rhs(A, flow), np.eye(A.shape[0]), T, N, m_F)[N]
+    return sequential_fine(make_rhs(A, flow), initial_state(A.shape[0], flow), T, N, m_F)[N]
+
+
+def accel_inverse(A: np.ndarray, E0, dt: float, steps: int, X0=None):
+    """Algorithm 8 (Example 5), literally:
+      X^(0) = X0; u^(0) = e (given, e ~ A^{-1} - X0);
+      for k: X^(k+1) = X^(k) + dt (I - A X^(k) + u^(k));  u^(k+1) = (I - dt A) u^(k).
+    Returns the list of iterates X^(0..steps)."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    I = np.eye(n)
+    X = np.zeros((n, n)) if X0 is None else np.asarray(X0, dtype=np.float64)
+    u = np.zeros((n, n)) if E0 is None else np.asarray(E0, dtype=np.float64)
+    out = [X]
+    for _ in range(steps):
+        X, u = X + dt * ((I - A @ X) + u), u - dt * (A @ u)
+        out.append(X)
+    return out
+
+
+def cosine_algorithm5(A: np.ndarray, N: int, m_G: int, m_F: int, K_max: int, tol: float = 0.0,
+                      stop: int = STOP_FIXED_K):
+    """Algorithm 5, steps in the paper's order:
+      1. the smallest non-negative integer m with 2^{-m} ||A||_inf <= 1;
+      2. A0 = 2^{-m} A;
+      3. C0 = cos(A0) by parareal on the trig block flow (eq. eqB, T = 1; classical parareal here);
+      4. C_{i+1} = 2 C_i^2 - I for i = 0..m-1;  X = C_m.
+    Returns (C_m, m, parareal output)."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    norm_inf = np.abs(A).sum(axis=1).max()
+    m = 0
+    while 2.0 ** (-m) * norm_inf > 1.0:
+        m += 1
+    A0 = A * 2.0 ** (-m)
+    out = solve(A0, FLOW_TRIG, 1.0, N, m_G, m_F, K_max, tol, stop)
+    C = out["X"][n:]
+    for _ in range(m):
+        C = 2.0 * (C @ C) - np.eye(n)
+    return C, m, out

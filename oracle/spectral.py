@@ -32,6 +32,8 @@ def scalar_rhs(lam, flow: int):
         return lambda x: lam - x * x
     if flow == dense.FLOW_EXP:
         return lambda x: lam * x
+    if flow == dense.FLOW_TRIG:       # state (s, c): s' = lam c, c' = -lam s  (eq. eqB per eigenvalue)
+        return lambda u: np.stack([lam * u[1], -(lam * u[0])])
     raise ValueError(flow)
 
 
@@ -41,12 +43,12 @@ def solve(eigvals: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, 
     dict shape with X/U entries as eigen-coefficient vectors u (reconstruct with `reconstruct`)."""
     lam = np.asarray(eigvals, dtype=np.float64)
     rhs = scalar_rhs(lam, flow)
-    x0 = np.ones_like(lam)
+    x0 = np.stack([np.zeros_like(lam), np.ones_like(lam)]) if flow == dense.FLOW_TRIG else np.ones_like(lam)
     norm = lambda u: float(np.sqrt(np.sum(u * u)))
     if flow == dense.FLOW_INVERSE:
         # ||A X - I||_F / sqrt(n) = ||lam u - 1||_2 / sqrt(n)
         residual = lambda u: norm(lam * u - 1.0) / math.sqrt(lam.size)
-    elif flow == dense.FLOW_EXP:
+    elif flow in (dense.FLOW_EXP, dense.FLOW_TRIG):
         residual = None
     else:
         # ||A - X^2||_F / ||A||_F = ||lam - u^2||_2 / ||lam||_2
@@ -56,7 +58,9 @@ def solve(eigvals: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, 
 
 
 def reconstruct(V: np.ndarray, u: np.ndarray) -> np.ndarray:
-    """V diag(u) V^T."""
+    """V diag(u) V^T (for a trig state (2, n): the stack [V diag(s) V^T; V diag(c) V^T])."""
+    if u.ndim == 2:
+        return np.vstack([(V * u[0]) @ V.T, (V * u[1]) @ V.T])
     return (V * u) @ V.T
 
 

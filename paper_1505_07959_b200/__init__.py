@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(HERE, "libmfode.so")
 FLOW_INVERSE = 0
 FLOW_SQRT = 1
 FLOW_EXP = 2
+FLOW_TRIG = 3      # state (sin, cos) stacked 2n x n (Example 3, eq. eqB)
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
@@ -35,7 +36,7 @@ EXPORTED = [
     "mfode_create", "mfode_create_device", "mfode_set_matrix", "mfode_parareal_solve", "mfode_sequential_fine",
     "mfode_residual", "mfode_get_result", "mfode_get_result_device", "mfode_get_slice", "mfode_set_option",
     "mfode_last_error", "mfode_destroy", "mfode_dgemm", "mfode_rk_stage", "mfode_frobenius", "mfode_partition",
-    "mfode_kernel_launches", "mfode_last_global_error", "mfode_version",
+    "mfode_kernel_launches", "mfode_last_global_error", "mfode_version", "mfode_cosine", "mfode_accel_inverse",
 ]
 
 
@@ -97,6 +98,9 @@ def lib() -> ctypes.CDLL:
         "mfode_kernel_launches": (ctypes.c_int64, []),
         "mfode_last_global_error": (ctypes.c_char_p, []),
         "mfode_version": (ctypes.c_char_p, []),
+        "mfode_cosine": (I, [P, I64, I, I, I, I, D, I, ctypes.POINTER(Dist), P, ctypes.POINTER(I),
+                             ctypes.POINTER(SolveInfo)]),
+        "mfode_accel_inverse": (I, [P, P, P, I64, D, I, D, I, P, ctypes.POINTER(I), ctypes.POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -259,6 +263,35 @@ def frobenius(X, Y=None, stream=None):
     _check(lib().mfode_frobenius(_ptr(X), _ptr(Y), n, ld, out,
                                  _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
     return out[0], out[1]
+
+
+def cosine(A: np.ndarray, N: int, m_G: int, m_F: int, K_max: int, tol: float = 0.0, stop: int = STOP_FIXED_K,
+           world: int = 1):
+    """Algorithm 5 through mfode_cosine: returns (cos(A), m, info)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    C = np.empty((n, n), dtype=np.float64)
+    m = ctypes.c_int()
+    info = SolveInfo()
+    dist = Dist(0, world, 0, None) if world > 1 else None
+    _check(lib().mfode_cosine(A.ctypes.data, n, N, m_G, m_F, K_max, tol, stop,
+                              ctypes.byref(dist) if dist else None, C.ctypes.data, ctypes.byref(m),
+                              ctypes.byref(info)))
+    return C, m.value, info.to_dict()
+
+
+def accel_inverse(A: np.ndarray, E0: Optional[np.ndarray], dt: float, max_steps: int, tol: float = 0.0,
+                  check_every: int = 0, X0: Optional[np.ndarray] = None):
+    """Algorithm 8 through mfode_accel_inverse: returns (X, steps, residual, status)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    X = np.empty((n, n), dtype=np.float64)
+    E0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
+    X0 = None if X0 is None else np.ascontiguousarray(X0, dtype=np.float64)
+    steps, res = ctypes.c_int(), ctypes.c_double()
+    st = _check(lib().mfode_accel_inverse(A.ctypes.data, _ptr(X0), _ptr(E0), n, dt, max_steps, tol, check_every,
+                                          X.ctypes.data, ctypes.byref(steps), ctypes.byref(res)))
+    return X, steps.value, res.value, _STATUS[st]
 
 
 def partition(N: int, world: int, rank: int):

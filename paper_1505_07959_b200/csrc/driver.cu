@@ -115,6 +115,7 @@ struct Rank {
 
 struct mfode_ctx {
   int n = 0, ld = 0, flow = 0, N = 0, mG = 1, mF = 1;
+  int ms = 1;                // matrices per state (2 for the trig block flow)
   double T = 1.0;
   int world = 1, device = 0;
   bool nccl_mode = false;
@@ -175,16 +176,22 @@ static int fail(mfode_ctx* h, int code, const char* fmt, ...) {
     if (s_ < 0) return s_;  \
   } while (0)
 
+// A state is `ms` consecutive n x ld matrices (ms = 2 for the trig block flow U = (X, Y), else 1).
 static inline size_t mat_elems(const mfode_ctx* h) { return (size_t)h->n * h->ld; }
-static inline double* slot(const mfode_ctx* h, double* slab, int j) { return slab + (size_t)j * mat_elems(h); }
+static inline size_t state_elems(const mfode_ctx* h) { return (size_t)h->ms * h->n * h->ld; }
+static inline double* slot(const mfode_ctx* h, double* slab, int j) { return slab + (size_t)j * state_elems(h); }
 
+// GEMMs per rhs evaluation: inverse X (B X) = 2; trig (A Y, -A X) = 2; sqrt, exp = 1
+static int rhs_gemms(const mfode_ctx* h) {
+  return (h->flow == MFODE_FLOW_INVERSE || h->flow == MFODE_FLOW_TRIG) ? 2 : 1;
+}
 static double rk4_flops(const mfode_ctx* h) {
   const double n3 = (double)h->n * h->n * h->n;
-  return (h->flow == MFODE_FLOW_INVERSE ? 16.0 : 8.0) * n3;
+  return 4.0 * rhs_gemms(h) * 2.0 * n3;
 }
 static double euler_flops(const mfode_ctx* h) {
   const double n3 = (double)h->n * h->n * h->n;
-  return (h->flow == MFODE_FLOW_INVERSE ? 4.0 : 2.0) * n3;
+  return rhs_gemms(h) * 2.0 * n3;
 }
 
 int partition(int N, int world, int rank, int* first, int* count) {
@@ -233,12 +240,22 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     p.beta = 1.0;
     p.C = MatRef{h->A, 0};
     CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Y, p, st));
-  } else {   // MFODE_FLOW_EXP: K = A Y
+  } else if (h->flow == MFODE_FLOW_EXP) {   // K = A Y
     if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
     p.alpha = 1.0;
     p.beta = 0.0;
     Operand Aop{h->A, 1, 0, 0};
     CUDA_TRY(h, launch_gemm(epi, h->tile, Aop, Y, p, st));
+  } else {   // MFODE_FLOW_TRIG: the batch runs over sub-matrices (X, Y) of each state:
+             // K_X = A Y (even z), K_Y = -A X (odd z)  -- eq. (eqB) P:448-456 with X0 = 0
+    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    p.alt_sign = 1;
+    Operand Aop{h->A, 1, 0, 0};
+    Operand Ysw = Y;
+    Ysw.xr = 1;
+    CUDA_TRY(h, launch_gemm(epi, h->tile, Aop, Ysw, p, st));
   }
   return MFODE_OK;
 }
@@ -251,30 +268,31 @@ static int coarse_G(mfode_ctx* h, Rank& R, const double* in_slab, int in_count, 
                     double* Xout, double* Gold, double* Fk, cudaEvent_t fk_ready) {
   const double hG = h->T / ((double)h->N * h->mG);
   const long long me = (long long)mat_elems(h);
+  const int ms = h->ms;
   const double* cur_slab = in_slab;
   int cur_count = in_count, cur_idx = in_idx;
   for (int i = 0; i < h->mG; ++i) {
     const bool last = (i == h->mG - 1);
-    GemmParams p = base_params(h, 1);
+    GemmParams p = base_params(h, ms);   // one state = ms sub-matrices
     p.h = hG;
-    p.X_in = MatRef{const_cast<double*>(cur_slab) + (size_t)cur_idx * me, 0};
+    p.X_in = MatRef{const_cast<double*>(cur_slab) + (size_t)cur_idx * ms * me, me};
     double* tmp = (i % 2 == 0) ? R.Xa : R.Xb;
     int epi;
     if (!last) {
       epi = EPI_EULER;
-      p.X_out = MatRef{tmp, 0};
+      p.X_out = MatRef{tmp, me};
     } else if (last_epi == EPI_EULER) {
       epi = EPI_EULER;
-      p.X_out = MatRef{Xout, 0};
-      p.Gold = MatRef{Gold, 0};
+      p.X_out = MatRef{Xout, me};
+      p.Gold = MatRef{Gold, me};
     } else {
       epi = EPI_EULER_CORR;
-      p.U_out = MatRef{Xout, 0};
-      p.Gold = MatRef{Gold, 0};
-      p.F_in = MatRef{Fk, 0};
+      p.U_out = MatRef{Xout, me};
+      p.Gold = MatRef{Gold, me};
+      p.F_in = MatRef{Fk, me};
     }
-    Operand Y{cur_slab, cur_count, cur_idx, 0};
-    TRY(flow_gemms(h, Y, R.Wc, 1, 1, p, epi, R.coarse, (last && last_epi == EPI_EULER_CORR) ? fk_ready : nullptr));
+    Operand Y{cur_slab, cur_count * ms, cur_idx * ms, 1};
+    TRY(flow_gemms(h, Y, R.Wc, 1, ms, p, epi, R.coarse, (last && last_epi == EPI_EULER_CORR) ? fk_ready : nullptr));
     cur_slab = tmp;
     cur_count = 1;
     cur_idx = 0;
@@ -293,14 +311,16 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
                                   hF, stop_flag, R.fine));
     return MFODE_OK;
   }
-  Operand Xu{R.U[par], R.nloc + 1, ja, 1};
-  Operand Xf{R.Fk, R.nloc, ja, 1};
-  Operand Ya{R.Ya, h->cap, 0, 1}, Yb{R.Yb, h->cap, 0, 1};
+  // batch index = sub-matrix index (ms per state)
+  const int ms = h->ms;
+  Operand Xu{R.U[par], (R.nloc + 1) * ms, ja * ms, 1};
+  Operand Xf{R.Fk, R.nloc * ms, ja * ms, 1};
+  Operand Ya{R.Ya, h->cap * ms, 0, 1}, Yb{R.Yb, h->cap * ms, 0, 1};
   for (int i = 0; i < h->mF; ++i) {
     const Operand& X = (i == 0) ? Xu : Xf;
     double* Xin = (i == 0) ? slot(h, R.U[par], ja) : slot(h, R.Fk, ja);
     for (int s = 1; s <= 4; ++s) {
-      GemmParams p = base_params(h, Z);
+      GemmParams p = base_params(h, Z * ms);
       p.stop_flag = stop_flag;
       p.stage = s;
       p.h = hF;
@@ -321,7 +341,7 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
         p.X_out = MatRef{slot(h, R.Fk, ja), me};
         p.Y_out = MatRef{nullptr, 0};
       }
-      TRY(flow_gemms(h, *Yin, R.W, h->cap, Z, p, EPI_RK, R.fine, nullptr));
+      TRY(flow_gemms(h, *Yin, R.W, h->cap, Z * ms, p, EPI_RK, R.fine, nullptr));
     }
   }
   return MFODE_OK;
@@ -333,7 +353,7 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
 static int fine_chunk_size(const mfode_ctx* h, int active) {
   if (h->small || active <= 1) return std::max(1, std::min(active, h->cap));
   const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, std::min(active, h->cap));
-  const long long t1 = gemm_tiles(tile, h->n, 1);
+  const long long t1 = gemm_tiles(tile, h->n, 1) * h->ms;   // tiles of one slice's GEMM launch
   const long long slots = 148LL * (tile == TILE_128 ? 1 : (tile == TILE_64 ? 2 : 4));
   const long long launches = (long long)h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
   const long long euler_gemms = (long long)h->mG * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
@@ -402,7 +422,7 @@ static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
 static int send_boundary(mfode_ctx* h, Rank& R, int par) {
   if (R.id >= h->world - 1) return MFODE_OK;
   if (h->nccl_mode) {
-    NCCL_TRY(h, nccl().send(slot(h, R.U[par], R.nloc), mat_elems(h), ncclFloat64, R.id + 1, h->comm, R.coarse));
+    NCCL_TRY(h, nccl().send(slot(h, R.U[par], R.nloc), state_elems(h), ncclFloat64, R.id + 1, h->comm, R.coarse));
   } else {
     // logical ranks: the receiver copies after the sender's event (recorded in evC[nloc-1])
   }
@@ -412,11 +432,11 @@ static int send_boundary(mfode_ctx* h, Rank& R, int par) {
 static int recv_boundary(mfode_ctx* h, Rank& R, int par) {
   if (R.id == 0) return MFODE_OK;
   if (h->nccl_mode) {
-    NCCL_TRY(h, nccl().recv(R.U[par], mat_elems(h), ncclFloat64, R.id - 1, h->comm, R.coarse));
+    NCCL_TRY(h, nccl().recv(R.U[par], state_elems(h), ncclFloat64, R.id - 1, h->comm, R.coarse));
   } else {
     Rank& P = h->ranks[R.id - 1];
     CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, P.evC[P.nloc - 1], 0));
-    CUDA_TRY(h, cudaMemcpyAsync(R.U[par], slot(h, P.U[par], P.nloc), mat_elems(h) * sizeof(double),
+    CUDA_TRY(h, cudaMemcpyAsync(R.U[par], slot(h, P.U[par], P.nloc), state_elems(h) * sizeof(double),
                                 cudaMemcpyDeviceToDevice, R.coarse));
   }
   return MFODE_OK;
@@ -506,7 +526,7 @@ static int enqueue_residual(mfode_ctx* h, Rank& R, const double* slab, int count
 }
 
 static int alloc_rank(mfode_ctx* h, Rank& R) {
-  const size_t me = mat_elems(h) * sizeof(double);
+  const size_t me = state_elems(h) * sizeof(double);   // bytes of one state (ms matrices)
   CUDA_TRY(h, cudaMalloc(&R.U[0], me * (R.nloc + 1)));
   CUDA_TRY(h, cudaMalloc(&R.U[1], me * (R.nloc + 1)));
   CUDA_TRY(h, cudaMalloc(&R.Fk, me * std::max(1, R.nloc)));
@@ -552,7 +572,7 @@ static int alloc_rank(mfode_ctx* h, Rank& R) {
 
 static void free_rank(mfode_ctx* h, Rank& R) {
   double* bufs[] = {R.U[0], R.U[1], R.Fk, R.Gold, R.Ya, R.Yb, R.W, R.S, R.Xa, R.Xb, R.Wc, R.partials, R.metric};
-  const size_t me = mat_elems(h);
+  const size_t me = state_elems(h);
   for (double* b : bufs)
     if (b) {
       forget_maps(b, b + me * (size_t)(std::max(R.nloc, h->cap) + 2));
@@ -592,7 +612,7 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   *out = nullptr;
   if (!A) return set_global_err(MFODE_EINVAL, "A is NULL");
   if (n < 1 || n > 65536) return set_global_err(MFODE_EINVAL, "n=%lld out of range [1, 65536]", (long long)n);
-  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT && flow != MFODE_FLOW_EXP)
+  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT && flow != MFODE_FLOW_EXP && flow != MFODE_FLOW_TRIG)
     return set_global_err(MFODE_EINVAL, "unknown flow %d", flow);
   if (!(T > 0.0) || !std::isfinite(T)) return set_global_err(MFODE_EINVAL, "T must be finite and > 0");
   if (N < 1 || mG < 1 || mF < 1) return set_global_err(MFODE_EINVAL, "N, coarse_steps, fine_steps must be >= 1");
@@ -607,7 +627,8 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   h->mG = mG;
   h->mF = mF;
   h->world = world;
-  h->small = (h->n <= kSmallMaxN);
+  h->ms = (flow == MFODE_FLOW_TRIG) ? 2 : 1;
+  h->small = (h->n <= kSmallMaxN) && h->ms == 1;
   int dev = 0;
   if (dist) dev = dist->device;
   else cudaGetDevice(&dev);
@@ -628,7 +649,7 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
     // Scratch for up to `cap` in-flight slices (3-4 matrices each) within a 16 GiB budget; the
     // chunk size actually used per sweep is chosen by fine_chunk_size() to minimise tile rounds.
     const int nloc_max = (N + world - 1) / world;
-    const double per_slice = 4.0 * 8.0 * (double)h->n * (double)h->ld;
+    const double per_slice = 4.0 * 8.0 * h->ms * (double)h->n * (double)h->ld;
     const int budget = (int)std::max(1.0, std::floor(16.0 * (1LL << 30) / per_slice));
     h->cap = std::max(1, std::min(nloc_max, budget));
   }
@@ -662,11 +683,13 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
       return set_global_err(s, "%s", e.c_str());
     }
   }
-  // X0 = I in slot 0 of both U buffers of rank 0 (logical or NCCL), once
+  // X0 = I in slot 0 of both U buffers of rank 0 (logical or NCCL), once.  Trig block flow:
+  // U(0) = (sin 0, cos 0) = (0, I) (eq. eqB with X0 = 0): the identity is sub-matrix 1.
   for (auto& R : hp->ranks)
     if (R.id == 0) {
-      launch_identity(R.U[0], hp->n, hp->ld, 1, 0, R.coarse);
-      launch_identity(R.U[1], hp->n, hp->ld, 1, 0, R.coarse);
+      const size_t off = (hp->flow == MFODE_FLOW_TRIG) ? mat_elems(hp) : 0;
+      launch_identity(R.U[0] + off, hp->n, hp->ld, 1, 0, R.coarse);
+      launch_identity(R.U[1] + off, hp->n, hp->ld, 1, 0, R.coarse);
     }
   cudaStream_t st = hp->ranks[0].coarse;
   if (!host && user_stream != (cudaStream_t)-1) {
@@ -711,7 +734,8 @@ static int first_bad_slice(mfode_ctx* h) {
     for (int j = 0; j <= R.nloc; ++j) {
       const int gidx = R.s0 + j;
       const int par = (gidx <= h->last_k ? gidx : h->last_k) % 2;
-      launch_frob(slot(h, R.U[par], j), nullptr, h->n, h->ld, R.partials, R.metric + 6, 1, 0.0, nullptr, R.coarse);
+      launch_frob(slot(h, R.U[par], j), nullptr, h->ms * h->n, h->ld, R.partials, R.metric + 6, 1, 0.0, nullptr,
+                  R.coarse);
       cudaMemcpyAsync(R.host_metric + 6, R.metric + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, R.coarse);
       cudaStreamSynchronize(R.coarse);
       if (!std::isfinite(R.host_metric[7])) return gidx;
@@ -722,8 +746,8 @@ static int first_bad_slice(mfode_ctx* h) {
 
 static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
   if (K_max < 0 || !(tol >= 0.0) || stop < 0 || stop > 2) return fail(h, MFODE_EINVAL, "bad K_max/tol/stop");
-  if (stop == MFODE_STOP_RESIDUAL && h->flow == MFODE_FLOW_EXP)
-    return fail(h, MFODE_EINVAL, "the exp flow has no residual stop test");
+  if (stop == MFODE_STOP_RESIDUAL && (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_TRIG))
+    return fail(h, MFODE_EINVAL, "the exp/trig flows have no residual stop test");
   CUDA_TRY(h, cudaSetDevice(h->device));
   const long long L0 = g_launches.load();
   const int K_eff = std::min(K_max, h->N);
@@ -772,7 +796,7 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
     int* flag = nullptr;
     if (owns_last(h)) {
       flag = (stop == MFODE_STOP_DELTA && spec && !h->nccl_mode) ? h->stop_flag : nullptr;
-      CUDA_TRY(h, launch_frob(slot(h, L.U[nxt], L.nloc), slot(h, L.U[cur], L.nloc), h->n, h->ld, L.partials,
+      CUDA_TRY(h, launch_frob(slot(h, L.U[nxt], L.nloc), slot(h, L.U[cur], L.nloc), h->ms * h->n, h->ld, L.partials,
                               L.metric + 0, 0, tol, flag, L.coarse));
       if (stop == MFODE_STOP_RESIDUAL) {
         int* rflag = (spec && !h->nccl_mode) ? h->stop_flag : nullptr;
@@ -906,7 +930,7 @@ static int sequential_impl(mfode_ctx* h, mfode_solve_info* info) {
     for (int j = 0; j < R.nloc && s == MFODE_OK; ++j) {
       s = fine_chunk(h, R, 0, j, j + 1, nullptr);
       if (s == MFODE_OK) {
-        cudaError_t e = cudaMemcpyAsync(slot(h, R.U[0], j + 1), slot(h, R.Fk, j), mat_elems(h) * sizeof(double),
+        cudaError_t e = cudaMemcpyAsync(slot(h, R.U[0], j + 1), slot(h, R.Fk, j), state_elems(h) * sizeof(double),
                                         cudaMemcpyDeviceToDevice, R.fine);
         if (e != cudaSuccess) s = fail(h, MFODE_ECUDA, "copy: %s", cudaGetErrorString(e));
       }
@@ -990,7 +1014,8 @@ int mfode_sequential_fine(mfode_ctx* h, mfode_solve_info* info) {
 int mfode_residual(mfode_ctx* h, double* rel) {
   if (!h || !rel) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!h->has_result) return fail(h, MFODE_EINVAL, "no result yet (call a solve first)");
-  if (h->flow == MFODE_FLOW_EXP) return fail(h, MFODE_EINVAL, "the exp flow has no residual");
+  if (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_TRIG)
+    return fail(h, MFODE_EINVAL, "the exp/trig flows have no residual");
   CUDA_TRY(h, cudaSetDevice(h->device));
   Rank& L = last_rank(h);
   if (owns_last(h)) {
@@ -1011,12 +1036,15 @@ static int get_result_impl(mfode_ctx* h, double* dst, bool host, cudaStream_t us
   if (h->nccl_mode) {
     // broadcast the result from the last rank into this rank's Xa scratch
     double* buf = L.Xa;
-    if (owns_last(h)) CUDA_TRY(h, cudaMemcpyAsync(buf, src, mat_elems(h) * sizeof(double), cudaMemcpyDeviceToDevice, L.coarse));
-    NCCL_TRY(h, nccl().bcast(buf, buf, mat_elems(h), ncclFloat64, h->world - 1, h->comm, L.coarse));
+    if (owns_last(h))
+      CUDA_TRY(h, cudaMemcpyAsync(buf, src, state_elems(h) * sizeof(double), cudaMemcpyDeviceToDevice, L.coarse));
+    NCCL_TRY(h, nccl().bcast(buf, buf, state_elems(h), ncclFloat64, h->world - 1, h->comm, L.coarse));
     src = buf;
   }
-  CUDA_TRY(h, cudaMemcpy2DAsync(dst, h->n * sizeof(double), src, h->ld * sizeof(double), h->n * sizeof(double), h->n,
-                                host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, L.coarse));
+  // the state's ms matrices are consecutive with equal stride, so one 2-D copy of ms*n rows
+  CUDA_TRY(h, cudaMemcpy2DAsync(dst, h->n * sizeof(double), src, h->ld * sizeof(double), h->n * sizeof(double),
+                                (size_t)h->ms * h->n, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                L.coarse));
   if (host) {
     CUDA_TRY(h, cudaStreamSynchronize(L.coarse));
   } else {
@@ -1046,7 +1074,7 @@ int mfode_get_slice(mfode_ctx* h, int n_index, double* U) {
     const int j = n_index - R.s0;
     const int par = h->seq_mode ? 0 : ((n_index <= h->last_k ? n_index : h->last_k) % 2);
     CUDA_TRY(h, cudaMemcpy2DAsync(U, h->n * sizeof(double), slot(h, R.U[par], j), h->ld * sizeof(double),
-                                  h->n * sizeof(double), h->n, cudaMemcpyDeviceToHost, R.coarse));
+                                  h->n * sizeof(double), (size_t)h->ms * h->n, cudaMemcpyDeviceToHost, R.coarse));
     CUDA_TRY(h, cudaStreamSynchronize(R.coarse));
     return MFODE_OK;
   }
@@ -1064,7 +1092,8 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     return MFODE_OK;
   }
   if (!strcmp(key, "small")) {
-    if (value && h->n > kSmallMaxN) return fail(h, MFODE_EINVAL, "small kernels need n <= %d", kSmallMaxN);
+    if (value && (h->n > kSmallMaxN || h->ms != 1))
+      return fail(h, MFODE_EINVAL, "small kernels need n <= %d and a one-matrix state", kSmallMaxN);
     h->small = value != 0;
     return MFODE_OK;
   }
@@ -1151,6 +1180,120 @@ int mfode_rk_stage(const double* dYop, const double* dBop, const double* dC, dou
   Operand A{dYop, 1, 0, 0}, B{dBop, 1, 0, 0};
   cudaError_t e = launch_gemm(EPI_RK, tile, A, B, p, (cudaStream_t)stream);
   if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "rk_stage: %s", cudaGetErrorString(e));
+  return MFODE_OK;
+}
+
+// Algorithm 5: m = min{m >= 0 : 2^-m ||A||_inf <= 1}; A0 = 2^-m A (exact in FP64);
+// C0 = cos(A0) = second block of the trig flow's state at T = 1 (classical parareal here; the paper
+// uses its modified variant); C_{i+1} = 2 C_i^2 - I, m times (one DMMA GEMM each: alpha = 2,
+// beta = -1, C = I).  Collective in NCCL mode; every rank receives C.
+int mfode_cosine(const double* A, int64_t n, int N_slices, int coarse_steps, int fine_steps, int K_max, double tol,
+                 int stop, const mfode_dist* dist, double* C, int* m_out, mfode_solve_info* info) {
+  if (!A || !C) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (n < 1 || n > 65536) return set_global_err(MFODE_EINVAL, "bad n");
+  double ninf = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j < n; ++j) s += fabs(A[i * n + j]);
+    ninf = std::max(ninf, s);
+  }
+  if (!std::isfinite(ninf)) return set_global_err(MFODE_EINVAL, "A is not finite");
+  int m = 0;
+  while (ldexp(ninf, -m) > 1.0) ++m;
+  std::vector<double> A0((size_t)n * n);
+  for (size_t i = 0; i < A0.size(); ++i) A0[i] = ldexp(A[i], -m);
+  mfode_ctx* h = nullptr;
+  int s = mfode_create(&h, A0.data(), n, MFODE_FLOW_TRIG, 1.0, N_slices, coarse_steps, fine_steps, dist);
+  if (s < 0) return s;
+  std::unique_ptr<mfode_ctx, void (*)(mfode_ctx*)> guard(h, mfode_destroy);
+  int st = mfode_parareal_solve(h, K_max, tol, stop, info);
+  if (st < 0) return set_global_err(st, "%s", h->err.c_str());
+  Rank& L = last_rank(h);
+  const size_t me = mat_elems(h);
+  double* cur = L.Xa;            // trig scratch holds 2 matrices: ping-pong Xa[0], Xa[1]
+  double* nxt = L.Xa + me;
+  double* I = L.Xb;              // identity
+  if (owns_last(h)) {
+    CUDA_TRY(h, cudaMemcpyAsync(cur, h->result_ptr + me, me * sizeof(double), cudaMemcpyDeviceToDevice, L.coarse));
+    CUDA_TRY(h, launch_identity(I, h->n, h->ld, 1, 0, L.coarse));
+    for (int i = 0; i < m; ++i) {
+      GemmParams p = base_params(h, 1);
+      p.alpha = 2.0;
+      p.beta = -1.0;
+      p.C = MatRef{I, 0};
+      p.Y_out = MatRef{nxt, 0};
+      Operand Cop{cur, 1, 0, 0};
+      CUDA_TRY(h, launch_gemm(EPI_STORE, h->tile, Cop, Cop, p, L.coarse));
+      std::swap(cur, nxt);
+    }
+  }
+  if (h->nccl_mode) NCCL_TRY(h, nccl().bcast(cur, cur, me, ncclFloat64, h->world - 1, h->comm, L.coarse));
+  CUDA_TRY(h, cudaMemcpy2DAsync(C, h->n * sizeof(double), cur, h->ld * sizeof(double), h->n * sizeof(double), h->n,
+                                cudaMemcpyDeviceToHost, L.coarse));
+  CUDA_TRY(h, cudaStreamSynchronize(L.coarse));
+  if (m_out) *m_out = m;
+  return st;
+}
+
+// Algorithm 8 (Example 5): dX/dt = I - A X with the accelerator u,
+//   X^{k+1} = X^k + dt (I - A X^k + u^k),  u^{k+1} = (I - dt A) u^k,  u^0 = e ~ A^{-1} - X^0.
+// The state (X, u) is two sub-matrices; one batched DMMA GEMM per step computes (A X, A u) and
+// the EPI_ACCEL epilogue applies both updates (out of place, ping-pong).  Sequential in k.
+int mfode_accel_inverse(const double* A, const double* X0, const double* E0, int64_t n, double dt, int max_steps,
+                        double tol, int check_every, double* X, int* steps_done, double* residual) {
+  if (!A || !X || max_steps < 0 || !(dt > 0.0) || !(tol >= 0.0) || check_every < 0)
+    return set_global_err(MFODE_EINVAL, "bad argument");
+  mfode_ctx* h = nullptr;
+  // one "slice" context (inverse-flow residual machinery; N = 1) owns A, the streams and scratch
+  int s = mfode_create(&h, A, n, MFODE_FLOW_INVERSE, 1.0, 1, 1, 1, nullptr);
+  if (s < 0) return s;
+  std::unique_ptr<mfode_ctx, void (*)(mfode_ctx*)> guard(h, mfode_destroy);
+  Rank& R = h->ranks[0];
+  const size_t me = mat_elems(h);
+  cudaStream_t st = R.coarse;
+  // state buffers: U[0] holds slots (X, u) -> use U[0] and U[1] (each >= 2 matrices: nloc+1 = 2)
+  double* cur = R.U[0];
+  double* nxt = R.U[1];
+  CUDA_TRY(h, cudaMemsetAsync(cur, 0, 2 * me * sizeof(double), st));
+  if (X0)
+    CUDA_TRY(h, cudaMemcpy2DAsync(cur, h->ld * sizeof(double), X0, n * sizeof(double), n * sizeof(double), n,
+                                  cudaMemcpyHostToDevice, st));
+  if (E0)
+    CUDA_TRY(h, cudaMemcpy2DAsync(cur + me, h->ld * sizeof(double), E0, n * sizeof(double), n * sizeof(double), n,
+                                  cudaMemcpyHostToDevice, st));
+  int k = 0;
+  double r = NAN;
+  while (k < max_steps) {
+    GemmParams p = base_params(h, 2);
+    p.h = dt;
+    p.X_in = MatRef{cur, (long long)me};
+    p.S = MatRef{cur + me, 0};          // even z reads u at the same position
+    p.X_out = MatRef{nxt, (long long)me};
+    Operand Aop{h->A, 1, 0, 0};
+    Operand Sop{cur, 2, 0, 1};
+    CUDA_TRY(h, launch_gemm(EPI_ACCEL, h->tile, Aop, Sop, p, st));
+    std::swap(cur, nxt);
+    ++k;
+    if (tol > 0.0 && check_every > 0 && (k % check_every == 0 || k == max_steps)) {
+      h->result_ptr = cur;
+      h->has_result = true;
+      TRY(enqueue_residual(h, R, cur, 1, 0, 2, 0.0, nullptr));
+      CUDA_TRY(h, cudaMemcpyAsync(R.host_metric + 2, R.metric + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(h, cudaStreamSynchronize(st));
+      r = R.host_metric[2];
+      if (!std::isfinite(r)) return fail(h, MFODE_ENONFINITE, "non-finite iterate at step %d", k);
+      if (r <= tol) break;
+    }
+  }
+  TRY(enqueue_residual(h, R, cur, 1, 0, 2, 0.0, nullptr));
+  CUDA_TRY(h, cudaMemcpyAsync(R.host_metric + 2, R.metric + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpy2DAsync(X, n * sizeof(double), cur, h->ld * sizeof(double), n * sizeof(double), n,
+                                cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  r = R.host_metric[2];
+  if (steps_done) *steps_done = k;
+  if (residual) *residual = r;
+  if (tol > 0.0 && !(r <= tol)) return MFODE_NOT_CONVERGED;
   return MFODE_OK;
 }
 

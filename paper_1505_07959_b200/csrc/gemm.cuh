@@ -39,7 +39,7 @@
 
 namespace mfode {
 
-enum Epi : int { EPI_STORE = 0, EPI_RK = 1, EPI_EULER = 2, EPI_EULER_CORR = 3, EPI_RESID = 4 };
+enum Epi : int { EPI_STORE = 0, EPI_RK = 1, EPI_EULER = 2, EPI_EULER_CORR = 3, EPI_RESID = 4, EPI_ACCEL = 5 };
 
 struct MatRef {           // element (z, r, c) at p[z * zstride + r * ld + c]
   double* p;
@@ -50,7 +50,9 @@ struct MatRef {           // element (z, r, c) at p[z * zstride + r * ld + c]
 struct GemmParams {
   int n, ld, num_z;
   int a_base, a_step;     // A-operand slice in its tensor map: a_base + z * a_step
-  int b_base, b_step;
+  int b_base, b_step;     // B-operand slice: b_base + (z ^ b_xor) * b_step
+  int b_xor;              // 1: pair sub-matrices (trig block flow: X' = A Y, Y' = -A X)
+  int alt_sign;           // 1: odd z use -alpha
   double alpha, beta;     // K = alpha * acc + beta * C
   MatRef C;               // read iff beta != 0
   MatRef X_in, X_out, S, Y_out, F_in, Gold, U_out;
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         const int m0 = (r / tiles_n) * BM;
         const int n0 = (r % tiles_n) * BN;
         const int sa = p.a_base + z * p.a_step;
-        const int sb = p.b_base + z * p.b_step;
+        const int sb = p.b_base + (z ^ p.b_xor) * p.b_step;
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     const int r = t - z * tiles_per_z;
     const int m0 = (r / tiles_n) * BM;
     const int n0 = (r % tiles_n) * BN;
+    const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
 
     double acc[Cfg::MT][2 * Cfg::NG][2];
 #pragma unroll
@@ -249,18 +252,18 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
           if (full4) {
             const double2 c0 = *reinterpret_cast<const double2*>(Cp);
             const double2 c1 = *reinterpret_cast<const double2*>(Cp + 2);
-            k4[0] = fma(p.alpha, k4[0], p.beta * c0.x);
-            k4[1] = fma(p.alpha, k4[1], p.beta * c0.y);
-            k4[2] = fma(p.alpha, k4[2], p.beta * c1.x);
-            k4[3] = fma(p.alpha, k4[3], p.beta * c1.y);
+            k4[0] = fma(alpha, k4[0], p.beta * c0.x);
+            k4[1] = fma(alpha, k4[1], p.beta * c0.y);
+            k4[2] = fma(alpha, k4[2], p.beta * c1.x);
+            k4[3] = fma(alpha, k4[3], p.beta * c1.y);
           } else {
             #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (e < cnt) k4[e] = fma(p.alpha, k4[e], p.beta * Cp[e]);
+              if (e < cnt) k4[e] = fma(alpha, k4[e], p.beta * Cp[e]);
           }
-        } else if (p.alpha != 1.0) {
+        } else if (alpha != 1.0) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) k4[e] *= p.alpha;
+          for (int e = 0; e < 4; ++e) k4[e] *= alpha;
         }
         double in0[4] = {0, 0, 0, 0}, in1[4] = {0, 0, 0, 0}, o0[4] = {0, 0, 0, 0}, o1[4] = {0, 0, 0, 0};
         if constexpr (EPI == EPI_STORE) {
@@ -286,10 +289,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
             for (int e = 0; e < 4; ++e) in0[e] = (e < cnt) ? Xp[e] : 0.0;
           }
           const double* Sp = nullptr;
-          if constexpr (EPI == EPI_RK) Sp = p.S.at(z) + off;
+          if constexpr (EPI == EPI_RK || EPI == EPI_ACCEL) Sp = p.S.at(z) + off;
           if constexpr (EPI == EPI_EULER_CORR) Sp = p.Gold.at(z) + off;
-          if constexpr (EPI == EPI_RK || EPI == EPI_EULER_CORR) {
-            if (EPI == EPI_EULER_CORR || p.stage > 1) {
+          if constexpr (EPI == EPI_RK || EPI == EPI_EULER_CORR || EPI == EPI_ACCEL) {
+            if (EPI == EPI_EULER_CORR || (EPI == EPI_RK && p.stage > 1) || (EPI == EPI_ACCEL && (z & 1) == 0)) {
               if (full4) {
                 const double2 a0 = *reinterpret_cast<const double2*>(Sp);
                 const double2 a1 = *reinterpret_cast<const double2*>(Sp + 2);
@@ -318,6 +321,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
           } else if constexpr (EPI == EPI_EULER) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) o0[e] = fma(p.h, k4[e], in0[e]);
+          } else if constexpr (EPI == EPI_ACCEL) {
+            // Algorithm 8: even z: X' = X + dt ((I - A X) + u); odd z: u' = u - dt A u
+            if ((z & 1) == 0) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) o0[e] = fma(p.h, (((row == col + e) ? 1.0 : 0.0) - k4[e]) + in1[e], in0[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) o0[e] = fma(-p.h, k4[e], in0[e]);
+            }
           } else if constexpr (EPI == EPI_EULER_CORR) {
             const double* Fp = p.F_in.at(z) + off;
             double fk[4];
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
             store4(p.S.at(z) + off, o1);
             store4(p.Y_out.at(z) + off, o0);
           }
-        } else if constexpr (EPI == EPI_EULER) {
+        } else if constexpr (EPI == EPI_EULER || EPI == EPI_ACCEL) {
           store4(p.X_out.at(z) + off, o0);
           if (p.Gold.p) store4(p.Gold.at(z) + off, o0);
         } else if constexpr (EPI == EPI_EULER_CORR) {

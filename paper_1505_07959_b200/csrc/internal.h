@@ -17,6 +17,7 @@ struct Operand {
   int count;
   int base;
   int step;
+  int xr = 0;   // B operand only: batch z reads matrix base + (z ^ xr) * step (trig block pairs)
 };
 
 extern std::atomic<long long> g_launches;

@@ -344,12 +344,14 @@ cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, G
   p.a_step = A.step;
   p.b_base = B.base;
   p.b_step = B.step;
+  p.b_xor = B.xr;
   switch (epi) {
     case EPI_STORE: return dispatch_tile<EPI_STORE>(tile, ma, mb, p, st);
     case EPI_RK: return dispatch_tile<EPI_RK>(tile, ma, mb, p, st);
     case EPI_EULER: return dispatch_tile<EPI_EULER>(tile, ma, mb, p, st);
     case EPI_EULER_CORR: return dispatch_tile<EPI_EULER_CORR>(tile, ma, mb, p, st);
     case EPI_RESID: return dispatch_tile<EPI_RESID>(tile, ma, mb, p, st);
+    case EPI_ACCEL: return dispatch_tile<EPI_ACCEL>(tile, ma, mb, p, st);
   }
   return cudaErrorInvalidValue;
 }

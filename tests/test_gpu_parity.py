@@ -333,6 +333,57 @@ def test_exp_flow_vs_oracle(n):
         s.residual()
 
 
+@pytest.mark.parametrize("n", [24, 130])
+def test_trig_flow_vs_oracle(n):
+    """§8(f) f1: trig block flow (Example 3, eq. eqB, X0 = 0) -- the 2n x n state (sin; cos) runs as
+    pairs of sub-matrices in one batched GEMM (K_X = A Y, K_Y = -A X)."""
+    import scipy.linalg
+    A = workloads.random_nonsymmetric(n, 7, scale=1.0)
+    N, mG, mF = 6, 2, 20
+    s = mf.Solver(A, mf.FLOW_TRIG, 1.0, N, mG, mF)
+    info = s.solve(N, 1e-13, mf.STOP_DELTA)
+    X = np.empty((2 * n, n))
+    s.result(X)
+    ref = dense.solve(A, dense.FLOW_TRIG, 1.0, N, mG, mF, N, 1e-13, dense.STOP_DELTA)
+    assert info["k_done"] == ref["k_done"]
+    assert relF(X, ref["X"]) <= 1e-12
+    assert np.abs(X[:n] - scipy.linalg.sinm(A)).max() < 1e-8
+    assert np.abs(X[n:] - scipy.linalg.cosm(A)).max() < 1e-8
+    s3 = mf.Solver(A, mf.FLOW_TRIG, 1.0, N, mG, mF, world=3)
+    i3 = s3.solve(N, 1e-13, mf.STOP_DELTA)
+    X3 = np.empty((2 * n, n))
+    s3.result(X3)
+    assert np.array_equal(X, X3) and i3["k_done"] == info["k_done"]
+
+
+def test_cosine_algorithm5_vs_oracle():
+    """Algorithm 5 end to end through mfode_cosine vs the oracle's step-by-step version."""
+    import scipy.linalg
+    n = 60
+    A = 0.8 * workloads.random_nonsymmetric(n, 6, scale=2.0)
+    C, m, info = mf.cosine(A, 8, 2, 30, 8, 1e-13, mf.STOP_DELTA)
+    Cref, mref, out = dense.cosine_algorithm5(A, 8, 2, 30, 8, 1e-13, dense.STOP_DELTA)
+    assert m == mref and info["k_done"] == out["k_done"]
+    assert relF(C, Cref) <= 1e-10
+    assert np.abs(C - scipy.linalg.cosm(A)).max() < 1e-8
+
+
+@pytest.mark.parametrize("n", [40, 150])
+def test_accel_inverse_vs_oracle(n):
+    """§8(f) f4: Algorithm 8 on the DMMA GEMM with the EPI_ACCEL epilogue vs the oracle's
+    literal loop; with tol the residual ||AX - I||/sqrt(n) is reported."""
+    w = workloads.random_spd(n, 11)
+    A = w.A / np.linalg.norm(w.A)
+    Ainv = np.linalg.inv(A)
+    E0 = np.where(np.abs(Ainv) >= 0.01 * np.abs(Ainv).max(), Ainv, 0.0)   # thresholded at 1 % (P:702)
+    dt, K = 0.1, 40
+    X, steps, res, status = mf.accel_inverse(A, E0, dt, K)
+    ref = dense.accel_inverse(A, E0, dt, K)[K]
+    assert steps == K
+    assert relF(X, ref) <= 1e-12
+    assert abs(res - dense.residual_inverse(A, ref)) <= 1e-9 * max(res, 1e-300) + 1e-14
+
+
 def test_small_kernels_logical_ranks_and_sequential():
     w = workloads.config(0)
     s1, i1, X1 = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 8, 1e-13, mf.STOP_DELTA)

@@ -293,6 +293,69 @@ def test_exp_flow_against_expm():
     assert np.abs(S[N] @ Sm[N] - np.eye(n)).max() < 1e-9
 
 
+def test_trig_flow_against_sinm_cosm():
+    """Example 3, eq. (eqB) with X0 = 0: U(1) = (sin A; cos A).  Sequential fine RK4
+    matches scipy's sinm/cosm (library definitions) within the RK4 error for a non-symmetric A, and
+    sin^2 + cos^2 = I; parareal at K = N equals the sequential fine run bitwise; the spectral oracle
+    (s' = lam c, c' = -lam s per eigenvalue) agrees with the dense one for a symmetric A."""
+    import scipy.linalg
+    n = 9
+    A = workloads.random_nonsymmetric(n, 4, scale=1.0)
+    N, mF = 5, 40
+    S = dense.sequential_fine(dense.make_rhs(A, dense.FLOW_TRIG), dense.initial_state(n, dense.FLOW_TRIG),
+                              1.0, N, mF)[N]
+    assert S.shape == (2 * n, n)
+    assert np.abs(S[:n] - scipy.linalg.sinm(A)).max() < 1e-9
+    assert np.abs(S[n:] - scipy.linalg.cosm(A)).max() < 1e-9
+    assert np.abs(S[:n] @ S[:n] + S[n:] @ S[n:] - np.eye(n)).max() < 1e-9
+    out = dense.solve(A, dense.FLOW_TRIG, 1.0, N, 1, mF, N)
+    assert np.array_equal(out["X"], S)
+    w = workloads.random_spd(12, 8)
+    d = dense.solve(w.A, dense.FLOW_TRIG, 1.0, 6, 2, 10, 3)
+    s = spectral.solve(w.eigvals, dense.FLOW_TRIG, 1.0, 6, 2, 10, 3)
+    ref = spectral.reconstruct(w.eigvecs, s["X"])
+    assert dense.frob(d["X"] - ref) / dense.frob(ref) < 1e-13
+
+
+def test_cosine_algorithm5():
+    """Algorithm 5: m = min{m : 2^-m ||A||_inf <= 1} (golden: ||A||_inf = 5 -> m = 3,
+    written out from the definition), A0 = 2^-m A, C0 = cos(A0) by parareal, C_{i+1} = 2C_i^2 - I.
+    Against scipy's cosm within the RK4 error amplified by the m doublings."""
+    import scipy.linalg
+    C, m, out = dense.cosine_algorithm5(np.diag([5.0, -2.0, 1.0]), 4, 1, 20, 4)
+    assert m == 3
+    np.testing.assert_allclose(np.diag(C), np.cos([5.0, -2.0, 1.0]), rtol=0, atol=1e-9)
+    n = 10
+    A = 0.8 * workloads.random_nonsymmetric(n, 6, scale=2.0)
+    C, m, out = dense.cosine_algorithm5(A, 6, 2, 30, 6)
+    assert m >= 1
+    assert np.abs(C - scipy.linalg.cosm(A)).max() < 1e-8
+
+
+def test_accel_inverse_closed_forms():
+    """Algorithm 8.  With E_k = A^{-1} - X_k and R = I - dt A the recursion gives
+    E_k = R^{k-1} (R - k dt I) E_0 when u_0 = E_0 exactly (the paper's Fig. ACC_MAT_GRAD2 case),
+    and E_k = R^k E_0 with no accelerator (u_0 = 0: forward Euler on dX/dt = I - AX)."""
+    w = workloads.random_spd(8, 9)
+    A = w.A / np.linalg.norm(w.A)          # rescaled by its Frobenius norm as in P:702
+    Ainv = np.linalg.inv(A)
+    n, dt, K = 8, 0.1, 25
+    R = np.eye(n) - dt * A
+    E0 = Ainv.copy()                        # X0 = 0
+    Xs = accel = dense.accel_inverse(A, E0, dt, K)
+    for k in (1, 5, 10, 25):
+        Ek = np.linalg.matrix_power(R, k - 1) @ (R - k * dt * np.eye(n)) @ E0
+        np.testing.assert_allclose(Ainv - Xs[k], Ek, rtol=0, atol=1e-11 * np.abs(Ainv).max())
+    Xn = dense.accel_inverse(A, None, dt, K)
+    for k in (1, 7, 25):
+        np.testing.assert_allclose(Ainv - Xn[k], np.linalg.matrix_power(R, k) @ E0, rtol=0,
+                                   atol=1e-11 * np.abs(Ainv).max())
+    # the accelerator helps: at t = k dt = 1 (P:613-618, xi(t) = min(t-1, 0) e) the exact-e error is
+    # -dt A R^9 E_0, far below the plain flow's R^10 E_0
+    k1 = int(round(1 / dt))
+    assert np.linalg.norm(Ainv - accel[k1]) < 0.2 * np.linalg.norm(Ainv - Xn[k1])
+
+
 def test_config_workloads_shapes():
     """workloads builds what BASELINE.json names (sizes, symmetry, spectra)."""
     for i in (0, 1, 2):
