@@ -128,6 +128,17 @@ MFODE_API int mfode_set_matrix(mfode_ctx *h, const double *A);
  * Returns OK, NOT_CONVERGED (result valid), ENONFINITE, ECUDA, ENCCL, EINVAL. */
 MFODE_API int mfode_parareal_solve(mfode_ctx *h, int K_max, double tol, int stop, mfode_solve_info *info);
 
+/* Modified parareal for the linear homogeneous flows (MFODE_FLOW_EXP, MFODE_FLOW_TRIG):
+ * Algorithm 3.  Each sweep enlarges S^k = span(S^{k-1} u {U^k_n}) with the global QR
+ * of Algorithm 2 (modified Gram-Schmidt in the Frobenius inner product; blocks with
+ * r_ii <= 1e-12 max(1, ||Z_i||_F) are eliminated), propagates only the NEW basis blocks with the
+ * fine propagator (batched, one image per block since the flows are autonomous on a uniform
+ * grid), then updates U^{k+1}_{n+1} = F(P U^{k+1}_n) + G((I - P) U^{k+1}_n) (eq. eq_update).
+ * max_basis (0 = (N+1)(min(K_max, N)+1)) caps the basis.  stop: FIXED_K or DELTA.  One rank.
+ * Returns as mfode_parareal_solve; EINVAL for nonlinear flows or world > 1. */
+MFODE_API int mfode_modified_parareal_solve(mfode_ctx *h, int K_max, double tol, int stop, int max_basis,
+                                            mfode_solve_info *info);
+
 /* The reference of P:180/P:189: S_0 = X0, S_{n+1} = F(S_n), n = 0..N-1 (sequential fine; equals
  * parareal at K = N bitwise).  Leaves the result where mfode_get_result reads it. */
 MFODE_API int mfode_sequential_fine(mfode_ctx *h, mfode_solve_info *info);

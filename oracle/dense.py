@@ -184,6 +184,96 @@ def parareal(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K_max: int
     return out
 
 
+def frob_inner(A, B) -> float:
+    """<A, B>_F = tr(B^T A)."""
+    return float(np.sum(np.asarray(A) * np.asarray(B)))
+
+
+def global_qr(Z: list, Q: list, rank_tol: float = 1e-12, passes: int = 2):
+    """Algorithm 2 (globalQR), extending an existing F-orthonormal family Q (the Remark
+    of Algorithm 3: the basis of S^k completes that of S^{k-1}).  For each block Z_i in order:
+    Q = Z_i; for j: r_ji = <Q, Q_j>_F, Q = Q - r_ji Q_j; r_ii = ||Q||_F; keep Q / r_ii unless
+    r_ii is zero -- read as r_ii <= rank_tol * max(1, ||Z_i||_F) (reading R16).
+    Floating-point reading R17: the j-loop runs `passes` = 2 times ("twice is enough"
+    reorthogonalisation).  In exact arithmetic the second pass subtracts exact zeros, so it is
+    Algorithm 2; in FP64 a single pass loses orthogonality once the iterates become nearly
+    dependent (they converge), and the modified parareal then diverges (tests pin both).
+    Returns the list of indices (into Z) of the kept blocks; Q is extended in place."""
+    kept = []
+    for i, Zi in enumerate(Z):
+        q = Zi
+        for _ in range(passes):
+            for Qj in Q:
+                r = frob_inner(q, Qj)
+                q = q - r * Qj
+        rii = frob(q)
+        if rii > rank_tol * max(1.0, frob(Zi)):
+            Q.append(q / rii)
+            kept.append(i)
+    return kept
+
+
+def modified_parareal(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K_max: int,
+                      tol: float = 0.0, stop: int = STOP_FIXED_K, rank_tol: float = 1e-12,
+                      keep_history: bool = False) -> dict:
+    """Algorithm 3: modified parareal for a linear homogeneous flow.
+      Step 0: U^0_{n+1} = G(U^0_n), U^0_0 = U_0; S^{-1} = {}.
+      Step k+1: S^k = span(S^{k-1} u {U^k_n, n = 0..N}) by globalQR (basis Q, completed);
+                F(Q_new) "in parallel" for the new blocks only (autonomous flow on a uniform grid:
+                one image per block serves every n);
+                U^{k+1}_{n+1} = F(P^k U^{k+1}_n) + G((I - P^k) U^{k+1}_n)          eq. (eq_update)
+                with P^k U = sum_i alpha_i Q_i, alpha = Q^T <> U, F(P U) = sum_i alpha_i F(Q_i).
+    """
+    hG = T / (N * m_G)
+    hF = T / (N * m_F)
+    G = lambda x: euler(rhs, x, hG, m_G)
+    F = lambda x: rk4(rhs, x, hF, m_F)
+    U = [X0]
+    for n in range(N):
+        U.append(G(U[n]))
+    Q, FQ = [], []
+    deltas = []
+    history = [list(U)] if keep_history else None
+    k_done = 0
+    converged = stop == STOP_FIXED_K
+    for k in range(min(K_max, N)):
+        nb_old = len(Q)
+        global_qr(U, Q, rank_tol)
+        for Qi in Q[nb_old:]:
+            FQ.append(F(Qi))
+        V = [X0]
+        for n in range(N):
+            alpha = [frob_inner(Qi, V[n]) for Qi in Q]
+            PV = sum(a * Qi for a, Qi in zip(alpha, Q))
+            FPV = sum(a * Fi for a, Fi in zip(alpha, FQ))
+            V.append(FPV + G(V[n] - PV))
+        delta = frob(V[N] - U[N]) / frob(V[N])
+        U = V
+        k_done = k + 1
+        deltas.append(delta)
+        if keep_history:
+            history.append(list(U))
+        if stop == STOP_DELTA and delta <= tol:
+            converged = True
+            break
+        if k_done == N:
+            converged = True
+            break
+    out = dict(X=U[N], U=U, k_done=k_done, deltas=deltas, converged=converged, basis=len(Q))
+    if keep_history:
+        out["history"] = history
+    return out
+
+
+def solve_modified(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,
+                   tol: float = 0.0, stop: int = STOP_FIXED_K, keep_history: bool = False) -> dict:
+    if flow not in (FLOW_EXP, FLOW_TRIG):
+        raise ValueError("Algorithm 3 is for linear homogeneous flows (exp, trig)")
+    A = np.asarray(A, dtype=np.float64)
+    return modified_parareal(make_rhs(A, flow), initial_state(A.shape[0], flow), T, N, m_G, m_F, K_max, tol,
+                             stop, keep_history=keep_history)
+
+
 def sequential_fine(rhs: Callable, X0, T: float, N: int, m_F: int) -> list:
     """The reference the paper compares against: S_0 = X0, S_{n+1} = F(S_n)."""
     hF = T / (N * m_F)

@@ -37,6 +37,7 @@ EXPORTED = [
     "mfode_residual", "mfode_get_result", "mfode_get_result_device", "mfode_get_slice", "mfode_set_option",
     "mfode_last_error", "mfode_destroy", "mfode_dgemm", "mfode_rk_stage", "mfode_frobenius", "mfode_partition",
     "mfode_kernel_launches", "mfode_last_global_error", "mfode_version", "mfode_cosine", "mfode_accel_inverse",
+    "mfode_modified_parareal_solve",
 ]
 
 
@@ -101,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "mfode_cosine": (I, [P, I64, I, I, I, I, D, I, ctypes.POINTER(Dist), P, ctypes.POINTER(I),
                              ctypes.POINTER(SolveInfo)]),
         "mfode_accel_inverse": (I, [P, P, P, I64, D, I, D, I, P, ctypes.POINTER(I), ctypes.POINTER(D)]),
+        "mfode_modified_parareal_solve": (I, [P, I, D, I, I, ctypes.POINTER(SolveInfo)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -200,6 +202,15 @@ class Solver:
     def solve(self, K_max: int, tol: float = 0.0, stop: int = STOP_FIXED_K) -> dict:
         info = SolveInfo()
         st = _check(lib().mfode_parareal_solve(self._h, K_max, tol, stop, ctypes.byref(info)), self._h)
+        d = info.to_dict()
+        d["status"] = _STATUS[st]
+        return d
+
+    def solve_modified(self, K_max: int, tol: float = 0.0, stop: int = STOP_FIXED_K, max_basis: int = 0) -> dict:
+        """Modified parareal, Algorithm 3 (linear homogeneous flows)."""
+        info = SolveInfo()
+        st = _check(lib().mfode_modified_parareal_solve(self._h, K_max, tol, stop, max_basis, ctypes.byref(info)),
+                    self._h)
         d = info.to_dict()
         d["status"] = _STATUS[st]
         return d

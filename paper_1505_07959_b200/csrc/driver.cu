@@ -131,6 +131,13 @@ struct mfode_ctx {
   int fine_batch_opt = 0;
   double normA = 0.0;        // ||A||_F
   std::vector<mfode::Rank> ranks;
+  // modified parareal (Algorithm 3): F-orthonormal basis Q of S^k, fine images F(Q), scratch
+  double* Qb = nullptr;
+  double* FQ = nullptr;
+  double* mtmp = nullptr;    // 3 states: P V, (I - P) V, G((I - P) V)
+  double* coef = nullptr;    // device coefficients (bcap + 8)
+  double* mpart = nullptr;   // multi-dot partials
+  int bcap = 0;
   // result
   int result_rank = -1;
   const double* result_ptr = nullptr;
@@ -300,25 +307,27 @@ static int coarse_G(mfode_ctx* h, Rank& R, const double* in_slab, int in_count, 
   return MFODE_OK;
 }
 
-// Fine propagator F on local slices [ja, jb) of rank R (batched), input U[par][j], output Fk[j].
-static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int* stop_flag) {
+// Fine propagator F (m_F RK4 steps) on Z = jb - ja states, batched: input states ja.. of the slab
+// `in` (in_count states), output states ja.. of the slab `out` (out_count states), in place.
+static int fine_prop(mfode_ctx* h, Rank& R, const double* in, int in_count, double* out, int out_count, int ja,
+                     int jb, const int* stop_flag) {
   const int Z = jb - ja;
   const double hF = h->T / ((double)h->N * h->mF);
   const long long me = (long long)mat_elems(h);
   if (h->small) {
     const double* M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
-    CUDA_TRY(h, launch_fine_small(h->flow, h->n, h->ld, M, slot(h, R.U[par], ja), slot(h, R.Fk, ja), me, Z, h->mF,
-                                  hF, stop_flag, R.fine));
+    CUDA_TRY(h, launch_fine_small(h->flow, h->n, h->ld, M, in + (size_t)ja * state_elems(h),
+                                  slot(h, out, ja), me, Z, h->mF, hF, stop_flag, R.fine));
     return MFODE_OK;
   }
   // batch index = sub-matrix index (ms per state)
   const int ms = h->ms;
-  Operand Xu{R.U[par], (R.nloc + 1) * ms, ja * ms, 1};
-  Operand Xf{R.Fk, R.nloc * ms, ja * ms, 1};
+  Operand Xu{in, in_count * ms, ja * ms, 1};
+  Operand Xf{out, out_count * ms, ja * ms, 1};
   Operand Ya{R.Ya, h->cap * ms, 0, 1}, Yb{R.Yb, h->cap * ms, 0, 1};
   for (int i = 0; i < h->mF; ++i) {
     const Operand& X = (i == 0) ? Xu : Xf;
-    double* Xin = (i == 0) ? slot(h, R.U[par], ja) : slot(h, R.Fk, ja);
+    double* Xin = (i == 0) ? const_cast<double*>(in) + (size_t)ja * state_elems(h) : slot(h, out, ja);
     for (int s = 1; s <= 4; ++s) {
       GemmParams p = base_params(h, Z * ms);
       p.stop_flag = stop_flag;
@@ -338,13 +347,18 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
         p.Y_out = MatRef{R.Ya, me};
       } else {
         Yin = &Ya;
-        p.X_out = MatRef{slot(h, R.Fk, ja), me};
+        p.X_out = MatRef{slot(h, out, ja), me};
         p.Y_out = MatRef{nullptr, 0};
       }
       TRY(flow_gemms(h, *Yin, R.W, h->cap, Z * ms, p, EPI_RK, R.fine, nullptr));
     }
   }
   return MFODE_OK;
+}
+
+// Fine propagator on local slices [ja, jb) of rank R: input U[par][j], output Fk[j].
+static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int* stop_flag) {
+  return fine_prop(h, R, R.U[par], R.nloc + 1, R.Fk, R.nloc, ja, jb, stop_flag);
 }
 
 // Slices per batched fine launch: balanced chunks whose total number of persistent-CTA tile
@@ -912,6 +926,176 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
   return MFODE_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Modified parareal for linear homogeneous flows (Algorithm 3)
+//   Step 0 as Algorithm 1.  Step k+1: S^k = span(S^{k-1} u {U^k_n}) with an F-orthonormal basis
+//   extended by the global QR of Algorithm 2 (modified Gram-Schmidt in <.,.>_F; a block
+//   with r_ii <= 1e-12 max(1, ||Z_i||_F) is eliminated -- reading R16); the fine images F(Q_i) of the
+//   NEW basis blocks only are propagated in parallel (batched); the update (eq. eq_update)
+//     U^{k+1}_{n+1} = sum_i alpha_i F(Q_i) + G(U^{k+1}_n - sum_i alpha_i Q_i),  alpha = Q^T <> U^{k+1}_n
+//   is sequential.  The flows are autonomous and the grid uniform, so F(T_{n+1}, T_n, .) is the same
+//   linear map for every n and one image per basis block suffices (SPEC design decision).
+// ---------------------------------------------------------------------------------------------
+static double host_frob(mfode_ctx* h, Rank& R, const double* X, const double* Y, cudaStream_t st, int* err) {
+  if (launch_frob(X, Y, h->ms * h->n, h->ld, R.partials, R.metric + 6, 1, 0.0, nullptr, st) != cudaSuccess ||
+      cudaMemcpyAsync(R.host_metric + 6, R.metric + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    *err = fail(h, MFODE_ECUDA, "frobenius failed");
+    return NAN;
+  }
+  return Y ? R.host_metric[6] : R.host_metric[7];
+}
+
+static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_basis, mfode_solve_info* info) {
+  if (K_max < 0 || !(tol >= 0.0) || (stop != MFODE_STOP_FIXED_K && stop != MFODE_STOP_DELTA))
+    return fail(h, MFODE_EINVAL, "bad K_max/tol/stop (modified parareal supports FIXED_K and DELTA)");
+  if (h->flow != MFODE_FLOW_EXP && h->flow != MFODE_FLOW_TRIG)
+    return fail(h, MFODE_EINVAL, "modified parareal (Algorithm 3) needs a linear homogeneous flow (exp, trig)");
+  if (h->world != 1) return fail(h, MFODE_EINVAL, "modified parareal runs on one rank");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const long long L0 = g_launches.load();
+  Rank& R = h->ranks[0];
+  const int N = h->N;
+  const size_t se = state_elems(h);
+  const int bcap = (max_basis > 0) ? max_basis : (N + 1) * (std::min(K_max, N) + 1);
+  if (bcap > h->bcap) {   // (re)allocate the basis storage
+    double* bufs[] = {h->Qb, h->FQ, h->mtmp};
+    for (double* b : bufs)
+      if (b) {
+        forget_maps(b, b + se * (size_t)(h->bcap + 3));
+        cudaFree(b);
+      }
+    if (h->coef) cudaFree(h->coef);
+    if (h->mpart) cudaFree(h->mpart);
+    h->Qb = h->FQ = h->mtmp = h->coef = h->mpart = nullptr;
+    h->bcap = 0;
+    CUDA_TRY(h, cudaMalloc(&h->Qb, se * bcap * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->FQ, se * bcap * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->mtmp, se * 3 * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->coef, (bcap + 8) * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->mpart, (size_t)std::min(bcap, 64) * 296 * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->Qb, 0, se * bcap * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->FQ, 0, se * bcap * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->mtmp, 0, se * 3 * sizeof(double)));
+    h->bcap = bcap;
+  }
+  cudaStream_t st = R.coarse;
+  CUDA_TRY(h, cudaStreamSynchronize(R.fine));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  mfode_solve_info loc;
+  memset(&loc, 0, sizeof(loc));
+  loc.bad_slice = -1;
+  loc.last_delta = NAN;
+  loc.residual = loc.residual0 = NAN;
+  loc.world = 1;
+  for (int i = 0; i < 64; ++i) loc.deltas[i] = NAN;
+  h->seq_mode = false;
+  h->has_result = false;
+  CUDA_TRY(h, cudaEventRecord(R.ev_t0, st));
+  CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_t0, 0));
+  TRY(enqueue_step0(h, R));   // U^0 in U[0]; slot 0 = X0 in both buffers
+  int nb = 0, err = MFODE_OK, k_done = 0, status = MFODE_OK;
+  bool converged = (stop == MFODE_STOP_FIXED_K);
+  double fine_solves = 0.0;
+  double* Wv = h->mtmp + se;
+  double* Gv = h->mtmp + 2 * se;
+  const int K_eff = std::min(K_max, N);
+  for (int k = 0; k < K_eff; ++k) {
+    const int cur = k % 2, nxt = (k + 1) % 2;
+    // (a) enhance the subspace with U^k_0..U^k_N: Algorithm 2 (MGS in <.,.>_F), new blocks appended
+    const int nb_old = nb;
+    for (int n = 0; n <= N && nb < h->bcap; ++n) {
+      const double* Z = slot(h, R.U[cur], n);
+      double* q = slot(h, h->Qb, nb);
+      CUDA_TRY(h, cudaMemcpyAsync(q, Z, se * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      const double zn = host_frob(h, R, Z, nullptr, st, &err);
+      TRY(err);
+      for (int pass = 0; pass < 2; ++pass)   // two passes: reading R17 (reorthogonalisation)
+        for (int j = 0; j < nb; ++j) {       // r_ji = <Q, Q_j>_F; Q = Q - r_ji Q_j
+          CUDA_TRY(h, launch_multidot(slot(h, h->Qb, j), (long long)se, 1, q, (long long)se, h->mpart, h->coef, st));
+          CUDA_TRY(h, launch_axpy_dev(q, slot(h, h->Qb, j), h->coef, (long long)se, 0, st));
+        }
+      const double rii = host_frob(h, R, q, nullptr, st, &err);
+      TRY(err);
+      if (!std::isfinite(rii)) {
+        status = MFODE_ENONFINITE;
+        loc.bad_slice = n;
+        break;
+      }
+      if (rii > 1e-12 * std::max(1.0, zn)) {   // keep: Q_i = Q / r_ii
+        CUDA_TRY(h, cudaMemcpyAsync(h->coef, &R.host_metric[7], sizeof(double), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(h, launch_axpy_dev(q, nullptr, h->coef, (long long)se, 1, st));
+        ++nb;
+      }
+    }
+    if (status < 0) break;
+    // (b) fine images of the new blocks, in parallel (batched over the blocks, chunks of `cap`)
+    if (nb > nb_old) {
+      CUDA_TRY(h, cudaEventRecord(R.ev_metric, st));
+      CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_metric, 0));
+      for (int ja = nb_old; ja < nb; ja += h->cap) {
+        const int jb = std::min(nb, ja + h->cap);
+        TRY(fine_prop(h, R, h->Qb, h->bcap, h->FQ, h->bcap, ja, jb, nullptr));
+      }
+      fine_solves += nb - nb_old;
+      CUDA_TRY(h, cudaEventRecord(R.ev_fine_end, R.fine));
+      CUDA_TRY(h, cudaStreamWaitEvent(st, R.ev_fine_end, 0));
+    }
+    // (c) sequential update (eq. eq_update): V_0 = X0
+    const double hG = h->T / ((double)N * h->mG);
+    (void)hG;
+    for (int n = 0; n < N; ++n) {
+      const double* V = slot(h, R.U[nxt], n);
+      CUDA_TRY(h, launch_multidot(h->Qb, (long long)se, nb, V, (long long)se, h->mpart, h->coef, st));
+      CUDA_TRY(h, launch_lincomb(Wv, h->Qb, (long long)se, h->coef, nb, (long long)se, V, -1.0, st));  // (I-P)V
+      TRY(coarse_G(h, R, Wv, 1, 0, EPI_EULER, Gv, nullptr, nullptr, nullptr));                        // G((I-P)V)
+      CUDA_TRY(h, launch_lincomb(slot(h, R.U[nxt], n + 1), h->FQ, (long long)se, h->coef, nb, (long long)se, Gv,
+                                 1.0, st));                                                            // + F(PV)
+    }
+    const double num = host_frob(h, R, slot(h, R.U[nxt], N), slot(h, R.U[cur], N), st, &err);
+    TRY(err);
+    const double den = R.host_metric[7];
+    const double delta = num / den;
+    k_done = k + 1;
+    h->last_k = k_done;
+    loc.last_delta = delta;
+    if (k < 64) loc.deltas[k] = delta;
+    if (!std::isfinite(delta)) {
+      status = MFODE_ENONFINITE;
+      break;
+    }
+    if (stop == MFODE_STOP_DELTA && delta <= tol) {
+      converged = true;
+      break;
+    }
+    if (k_done == N) {
+      converged = true;
+      break;
+    }
+  }
+  if (K_eff == 0) h->last_k = 0;
+  CUDA_TRY(h, cudaEventRecord(R.ev_t1, st));
+  CUDA_TRY(h, cudaEventSynchronize(R.ev_t1));
+  float ms = 0.f;
+  CUDA_TRY(h, cudaEventElapsedTime(&ms, R.ev_t0, R.ev_t1));
+  loc.ms_total = ms;
+  loc.k_done = k_done;
+  loc.converged = converged ? 1 : 0;
+  loc.fine_flops = fine_solves * h->mF * rk4_flops(h);
+  loc.coarse_flops = (double)N * (k_done + 1) * h->mG * euler_flops(h);
+  loc.gpu_launches = (int)(g_launches.load() - L0);
+  h->result_rank = 0;
+  h->result_ptr = slot(h, R.U[k_done % 2], R.nloc);
+  h->has_result = true;
+  if (info) *info = loc;
+  if (status < 0) return fail(h, status, "non-finite state in the modified parareal");
+  if (!converged) {
+    h->err = "not converged within K_max sweeps";
+    return MFODE_NOT_CONVERGED;
+  }
+  return MFODE_OK;
+}
+
 static int sequential_impl(mfode_ctx* h, mfode_solve_info* info) {
   CUDA_TRY(h, cudaSetDevice(h->device));
   const long long L0 = g_launches.load();
@@ -1004,6 +1188,12 @@ int mfode_set_matrix(mfode_ctx* h, const double* A) {
 int mfode_parareal_solve(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
   if (!h) return set_global_err(MFODE_EINVAL, "NULL handle");
   return solve_impl(h, K_max, tol, stop, info);
+}
+
+int mfode_modified_parareal_solve(mfode_ctx* h, int K_max, double tol, int stop, int max_basis,
+                                  mfode_solve_info* info) {
+  if (!h) return set_global_err(MFODE_EINVAL, "NULL handle");
+  return modified_impl(h, K_max, tol, stop, max_basis, info);
 }
 
 int mfode_sequential_fine(mfode_ctx* h, mfode_solve_info* info) {
@@ -1132,6 +1322,14 @@ void mfode_destroy(mfode_ctx* h) {
     cudaFree(h->B);
   }
   if (h->stop_flag) cudaFree(h->stop_flag);
+  double* mbufs[] = {h->Qb, h->FQ, h->mtmp};
+  for (double* b : mbufs)
+    if (b) {
+      forget_maps(b, b + state_elems(h) * (size_t)(h->bcap + 3));
+      cudaFree(b);
+    }
+  if (h->coef) cudaFree(h->coef);
+  if (h->mpart) cudaFree(h->mpart);
   if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
   delete h;
 }

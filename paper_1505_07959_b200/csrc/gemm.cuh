@@ -146,7 +146,33 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         const int n0 = (r % tiles_n) * BN;
         const int sa = p.a_base + z * p.a_step;
         const int sb = p.b_base + (z ^ p.b_xor) * p.b_step;
+        // Epilogue operands of this tile (X, S, C, F, Gold rows) are prefetched into L2 during the
+        // last k-steps, so the fused epilogue reads L2 instead of stalling every warp on HBM.
+        const int pf_k0 = KT > 8 ? KT - 8 : 0;
+        const int pf_bytes = (((n - n0) < BN ? (n - n0) : BN) * 8 + 15) & ~15;
+        const long long zoff = (long long)z;
         for (int kt = 0; kt < KT; ++kt) {
+          if (kt >= pf_k0) {
+            const int per = (BM + (KT - pf_k0) - 1) / (KT - pf_k0);
+            const int r0 = (kt - pf_k0) * per;
+            const int r1 = (r0 + per < BM) ? r0 + per : BM;
+            for (int rr = r0; rr < r1 && m0 + rr < n; ++rr) {
+              const long long off = (long long)(m0 + rr) * p.ld + n0;
+              if (p.beta != 0.0) prefetch_l2(p.C.at((int)zoff) + off, pf_bytes);
+              if constexpr (EPI == EPI_RK || EPI == EPI_EULER || EPI == EPI_EULER_CORR || EPI == EPI_ACCEL)
+                prefetch_l2(p.X_in.at((int)zoff) + off, pf_bytes);
+              if constexpr (EPI == EPI_RK) {
+                if (p.stage > 1) prefetch_l2(p.S.at((int)zoff) + off, pf_bytes);
+              }
+              if constexpr (EPI == EPI_ACCEL) {
+                if ((z & 1) == 0) prefetch_l2(p.S.at((int)zoff) + off, pf_bytes);
+              }
+              if constexpr (EPI == EPI_EULER_CORR) {
+                prefetch_l2(p.F_in.at((int)zoff) + off, pf_bytes);
+                prefetch_l2(p.Gold.at((int)zoff) + off, pf_bytes);
+              }
+            }
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
           unsigned char* sB = sA + Cfg::kABytes;

@@ -31,6 +31,15 @@ cudaError_t launch_frob(const double* X, const double* Y, int n, int ld, double*
 cudaError_t launch_reduce_partials(const double* partials, int count, double denom, double* out, double tol,
                                    int* stop_flag, cudaStream_t st);
 cudaError_t launch_copy_flag(const double* metric, double tol, int* stop_flag, cudaStream_t st);
+// Frobenius subspace algebra (modified parareal, §3): out[i] = <Q_i, V>_F (device); partials >= count*296
+cudaError_t launch_multidot(const double* Q, long long qstride, int count, const double* V, long long total,
+                            double* partials, double* out, cudaStream_t st);
+// out = add + sign * sum_i coef[i] Q_i (coef on the device, ascending i)
+cudaError_t launch_lincomb(double* out, const double* Q, long long qstride, const double* coef, int count,
+                           long long total, const double* add, double sign, cudaStream_t st);
+// Y -= coef[0] X, or (divide) Y /= coef[0]
+cudaError_t launch_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide,
+                            cudaStream_t st);
 cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
 int choose_tile(int n, int num_z);
 long long gemm_tiles(int tile, int n, int num_z);

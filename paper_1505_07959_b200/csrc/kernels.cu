@@ -143,6 +143,106 @@ __global__ void k_copy_flag(const double* metric, double tol, int* stop_flag) {
   *stop_flag = (*metric <= tol) ? 1 : 0;
 }
 
+// ---- Frobenius subspace algebra of the modified parareal (§3) -------------------------
+// multi-dot: partials[i * gridDim.x + b] = sum over block b's fixed share of Q_i . V, i < count.
+// V is read once per block share, every Q_i once (HBM traffic (count + 1) * elems).
+constexpr int kMaxDots = 64;   // coefficients per multi-dot pass (the driver loops over passes)
+
+__global__ void __launch_bounds__(kRedThreads) k_multidot(const double* Q, long long qstride, int count,
+                                                          const double* V, long long total, double* partials) {
+  double acc[kMaxDots];
+#pragma unroll
+  for (int i = 0; i < kMaxDots; ++i) acc[i] = 0.0;
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; e < total;
+       e += (long long)gridDim.x * blockDim.x * 2) {
+    const double2 v = *reinterpret_cast<const double2*>(V + e);
+#pragma unroll
+    for (int i = 0; i < kMaxDots; ++i) {
+      if (i < count) {
+        const double2 q = *reinterpret_cast<const double2*>(Q + i * qstride + e);
+        acc[i] = fma(q.x, v.x, acc[i]);
+        acc[i] = fma(q.y, v.y, acc[i]);
+      }
+    }
+  }
+  __shared__ double red[kRedThreads / 32];
+  for (int i = 0; i < count; ++i) {
+    double a = acc[0];
+    // rotate so that acc[0] holds coefficient i (keeps acc[] in registers: constant indices only)
+#pragma unroll
+    for (int j = 0; j < kMaxDots - 1; ++j) acc[j] = acc[j + 1];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kRedThreads / 32; ++w) s += red[w];
+      partials[(long long)i * gridDim.x + blockIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// out[i] = sum_b partials[i * blocks + b] (fixed order), one block per i
+__global__ void k_reduce_rows(const double* partials, int blocks, double* out) {
+  __shared__ double s0[32];
+  double a = 0.0;
+  for (int b = threadIdx.x; b < blocks; b += blockDim.x) a += partials[(long long)blockIdx.x * blocks + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) s0[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) x += s0[w];
+    out[blockIdx.x] = x;
+  }
+}
+
+// out = add + sign * sum_{i < count} coef[i] * Q_i   (ascending i; add may be null)
+__global__ void k_lincomb(double* out, const double* Q, long long qstride, const double* coef, int count,
+                          long long total, const double* add, double sign) {
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; e < total;
+       e += (long long)gridDim.x * blockDim.x * 2) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = 0; i < count; ++i) {
+      const double c = coef[i];
+      const double2 q = *reinterpret_cast<const double2*>(Q + i * qstride + e);
+      s.x = fma(c, q.x, s.x);
+      s.y = fma(c, q.y, s.y);
+    }
+    double2 r;
+    if (add) {
+      const double2 a = *reinterpret_cast<const double2*>(add + e);
+      r.x = fma(sign, s.x, a.x);
+      r.y = fma(sign, s.y, a.y);
+    } else {
+      r.x = sign * s.x;
+      r.y = sign * s.y;
+    }
+    *reinterpret_cast<double2*>(out + e) = r;
+  }
+}
+
+// Y = (Y - coef[0] * X) (axpy with a device scalar) or, with scale != 0, Y = Y / coef[0]
+__global__ void k_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide) {
+  const double c = *coef;
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; e < total;
+       e += (long long)gridDim.x * blockDim.x * 2) {
+    double2 y = *reinterpret_cast<double2*>(Y + e);
+    if (divide) {
+      y.x = y.x / c;
+      y.y = y.y / c;
+    } else {
+      const double2 x = *reinterpret_cast<const double2*>(X + e);
+      y.x = fma(-c, x.x, y.x);
+      y.y = fma(-c, x.y, y.y);
+    }
+    *reinterpret_cast<double2*>(Y + e) = y;
+  }
+}
+
 // --------------------------------------------------------------------------------------------
 // host wrappers
 // --------------------------------------------------------------------------------------------
@@ -178,6 +278,34 @@ cudaError_t launch_frob(const double* X, const double* Y, int n, int ld, double*
 cudaError_t launch_reduce_partials(const double* partials, int count, double denom, double* out,
                                    double tol, int* stop_flag, cudaStream_t st) {
   k_reduce_final<<<1, 1024, 0, st>>>(partials, count, 1, 2, denom, out, tol, stop_flag);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+constexpr int kDotBlocks = 296;
+
+// out[i] = <Q_i, V>_F for i < count (device), fixed reduction order; partials: count * kDotBlocks
+cudaError_t launch_multidot(const double* Q, long long qstride, int count, const double* V, long long total,
+                            double* partials, double* out, cudaStream_t st) {
+  for (int i0 = 0; i0 < count; i0 += kMaxDots) {
+    const int c = std::min(kMaxDots, count - i0);
+    k_multidot<<<kDotBlocks, kRedThreads, 0, st>>>(Q + i0 * qstride, qstride, c, V, total, partials);
+    k_reduce_rows<<<c, 256, 0, st>>>(partials, kDotBlocks, out + i0);
+    g_launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb(double* out, const double* Q, long long qstride, const double* coef, int count,
+                           long long total, const double* add, double sign, cudaStream_t st) {
+  k_lincomb<<<ew_grid(total), 256, 0, st>>>(out, Q, qstride, coef, count, total, add, sign);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide,
+                            cudaStream_t st) {
+  k_axpy_dev<<<ew_grid(total), 256, 0, st>>>(Y, X, coef, total, divide);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -69,6 +69,12 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// bulk L2 prefetch of `bytes` (multiple of 16) at a 16-byte aligned global address
+__device__ __forceinline__ void prefetch_l2(const void* gptr, int bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<uint64_t>(gptr)), "r"(bytes)
+               : "memory");
+}
+
 // ---- FP64 tensor core: mma.sync m8n8k4 (SASS DMMA.8x8x4) ---------------------------------------
 // A 8x4 row: lane holds A[lane>>2][lane&3]; B 4x8 col: lane holds B[lane&3][lane>>2];
 // C/D 8x8: lane holds C[lane>>2][2*(lane&3) + {0,1}].

@@ -384,6 +384,30 @@ def test_accel_inverse_vs_oracle(n):
     assert abs(res - dense.residual_inverse(A, ref)) <= 1e-9 * max(res, 1e-300) + 1e-14
 
 
+@pytest.mark.parametrize("flow,n", [(mf.FLOW_TRIG, 8), (mf.FLOW_TRIG, 100), (mf.FLOW_EXP, 40)])
+def test_modified_parareal_vs_oracle(flow, n):
+    """§8(f) f2: Algorithm 3 on the GPU (Frobenius MGS x2, batched fine images of new
+    basis blocks, sequential projected update) vs the oracle; both reach the sequential fine
+    solution once the basis saturates, far ahead of classical parareal."""
+    w = workloads.random_spd(n, 12, lo=0.5, hi=3.0)
+    N, mG, mF, K = 10, 1, 10, 3
+    s = mf.Solver(w.A, flow, 1.0, N, mG, mF)
+    info = s.solve_modified(K)
+    rows = 2 * n if flow == mf.FLOW_TRIG else n
+    X = np.empty((rows, n))
+    s.result(X)
+    ref = dense.solve_modified(w.A, flow, 1.0, N, mG, mF, K)
+    seq = dense.solve_sequential_fine(w.A, flow, 1.0, N, mF)
+    assert info["k_done"] == K
+    err_gpu = relF(X, seq)
+    err_ref = relF(ref["X"], seq)
+    assert relF(X, ref["X"]) <= 1e-10 or (err_gpu <= 1e-10 and err_ref <= 1e-10)
+    c = s.solve(K)
+    Xc = np.empty((rows, n))
+    s.result(Xc)
+    assert err_gpu <= relF(Xc, seq) + 1e-14
+
+
 def test_small_kernels_logical_ranks_and_sequential():
     w = workloads.config(0)
     s1, i1, X1 = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 8, 1e-13, mf.STOP_DELTA)

@@ -356,6 +356,69 @@ def test_accel_inverse_closed_forms():
     assert np.linalg.norm(Ainv - accel[k1]) < 0.2 * np.linalg.norm(Ainv - Xn[k1])
 
 
+def test_global_qr_examples_and_orthonormality():
+    """Algorithm 2: SPEC S:63-66 worked examples (diag(3,4) -> r_11 = 5; a dependent
+    block 2 Z1 is eliminated), and on random blocks Q^T <> Q = I and Z_i in span(Q) (Proposition)."""
+    Z1 = np.diag([3.0, 4.0])
+    Q = []
+    assert dense.global_qr([Z1], Q) == [0]
+    np.testing.assert_allclose(Q[0], Z1 / 5.0, rtol=0, atol=1e-16)
+    Q = []
+    assert dense.global_qr([Z1, 2.0 * Z1], Q) == [0]
+    rng = np.random.default_rng(3)
+    Z = [rng.standard_normal((6, 2)) for _ in range(4)]
+    Q = []
+    dense.global_qr(Z, Q)
+    G = np.array([[dense.frob_inner(a, b) for b in Q] for a in Q])
+    np.testing.assert_allclose(G, np.eye(len(Q)), rtol=0, atol=1e-12)
+    for Zi in Z:
+        P = sum(dense.frob_inner(Zi, q) * q for q in Q)
+        assert dense.frob(Zi - P) < 1e-12 * dense.frob(Zi)
+
+
+def test_modified_parareal_saturated_basis_is_fine():
+    """Algorithm 3: every iterate is a polynomial in A (X0 = I), so once S^k contains
+    span{I, A, ..., A^{n-1}} the projection is the identity on the iterates and eq. (eq_update)
+    reproduces the sequential fine propagation.  n = 3, N = 4: the Step-0 iterates I, G(I), ...
+    already span it, so sweep 1 equals the sequential fine solution up to rounding."""
+    n = 3
+    A = workloads.random_nonsymmetric(n, 8, scale=1.0)
+    out = dense.solve_modified(A, dense.FLOW_EXP, 1.0, 4, 1, 10, 1)
+    seq = dense.solve_sequential_fine(A, dense.FLOW_EXP, 1.0, 4, 10)
+    assert out["basis"] == n
+    assert dense.frob(out["X"] - seq) <= 1e-12 * dense.frob(seq)
+
+
+def test_modified_converges_faster_than_classical():
+    """P:489-490 (Fig. "cos": "the modified parareal algorithm converges much faster"): on the trig
+    block flow, the error against the sequential fine solution after k sweeps is never larger for
+    Algorithm 3 than for Algorithm 1 (SPEC S:223 monotone dominance), and strictly smaller at k = 2."""
+    n = 8
+    w = workloads.random_spd(n, 12, lo=0.5, hi=3.0)
+    N, mG, mF = 10, 1, 10
+    seq = dense.solve_sequential_fine(w.A, dense.FLOW_TRIG, 1.0, N, mF)
+    errs = []
+    for k in (1, 2, 3):
+        c = dense.solve(w.A, dense.FLOW_TRIG, 1.0, N, mG, mF, k)
+        m = dense.solve_modified(w.A, dense.FLOW_TRIG, 1.0, N, mG, mF, k)
+        errs.append((dense.frob(c["X"] - seq), dense.frob(m["X"] - seq)))
+        assert errs[-1][1] <= errs[-1][0] * (1 + 1e-9) + 1e-14
+    assert errs[1][1] < 0.5 * errs[1][0]
+    # the trig states (p(A), q(A)) span at most 2n dimensions: once S^k holds them the update is the
+    # fine propagation itself (rounding level), while classical parareal is still at ~1e-3
+    assert errs[2][1] < 1e-11 * dense.frob(seq) and errs[2][0] > 1e-5 * dense.frob(seq)
+    # R17: with a single Gram-Schmidt pass the same run loses orthogonality and diverges
+    rhs = dense.make_rhs(w.A, dense.FLOW_TRIG)
+    import oracle.dense as od
+    orig = od.global_qr
+    try:
+        od.global_qr = lambda Z, Q, rank_tol=1e-12: orig(Z, Q, rank_tol, passes=1)
+        one = od.modified_parareal(rhs, dense.initial_state(n, dense.FLOW_TRIG), 1.0, N, mG, mF, 3)
+    finally:
+        od.global_qr = orig
+    assert dense.frob(one["X"] - seq) > 1e3 * errs[2][1]
+
+
 def test_config_workloads_shapes():
     """workloads builds what BASELINE.json names (sizes, symmetry, spectra)."""
     for i in (0, 1, 2):
