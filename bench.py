@@ -137,6 +137,7 @@ def main():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sym-steps", type=int, default=1, help="timed solves of the f3 symmetric variant (0: skip)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -243,6 +244,35 @@ def main():
     e2e_value = e2e_flops / (e2e_ms * 1e-3) / 1e12 if args.e2e_steps > 0 else None
     resid = solver.residual()
 
+    # f3(i) symmetric variant, reported beside (never folded into) value: A = A^T, so every GEMM
+    # computes only its upper-triangle tiles and mirrors them (half the executed flops).
+    sym = None
+    if args.sym_steps > 0:
+        try:
+            solver.set_option("symmetric", 1)
+            solver.solve(w.K_max, w.tol, w.stop)      # warm-up
+            barrier()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            sinfos = [solver.solve(w.K_max, w.tol, w.stop) for _ in range(args.sym_steps)]
+            s1.record()
+            s1.synchronize()
+            sms = s0.elapsed_time(s1) / args.sym_steps
+            if world > 1:
+                t = torch.tensor([sms], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                sms = float(t.item())
+            sres = solver.residual()
+            solver.set_option("symmetric", 0)
+            ffl = float(np.mean([i["fine_flops"] for i in sinfos]))
+            sym = {"time_to_tol_ms": sms, "k_done": sinfos[-1]["k_done"], "residual": sres,
+                   "algorithmic_fine_tflops": ffl / (sms * 1e-3) / 1e12,
+                   "executed_fine_tflops_approx": ffl * (w.n // 128 + 1) / (2 * (w.n // 128)) / (sms * 1e-3) / 1e12,
+                   "speedup_vs_full": ms_step / sms}
+        except Exception as e:   # noqa: BLE001
+            sym = {"error": str(e)}
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -274,6 +304,7 @@ def main():
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "cublas_dgemm_4096_tflops": cublas},
             "cpu_baseline": cpu,
+            "f3_symmetric_variant": sym,
         }
         print(json.dumps(line), flush=True)
     solver.close()

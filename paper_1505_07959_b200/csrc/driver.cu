@@ -127,6 +127,8 @@ struct mfode_ctx {
   int cap = 1;               // fine batch capacity (slices per launch)
   int tile = 0;              // 0 auto
   bool small = false;        // K6 shared-memory kernels (n <= kSmallMaxN)
+  bool sym = false;          // f3: symmetric GEMMs (upper tiles + mirror), needs A == A^T exactly
+  bool a_symmetric = false;  // A == A^T bitwise (checked at load)
   bool overlap = true;
   int fine_batch_opt = 0;
   double normA = 0.0;        // ||A||_F
@@ -220,6 +222,7 @@ static GemmParams base_params(const mfode_ctx* h, int num_z) {
   p.num_z = num_z;
   p.alpha = 1.0;
   p.beta = 0.0;
+  p.sym = h->sym ? 1 : 0;
   return p;
 }
 
@@ -366,8 +369,8 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
 // partial round of every launch is idle tensor time.  Ties go to larger chunks (fewer launches).
 static int fine_chunk_size(const mfode_ctx* h, int active) {
   if (h->small || active <= 1) return std::max(1, std::min(active, h->cap));
-  const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, std::min(active, h->cap));
-  const long long t1 = gemm_tiles(tile, h->n, 1) * h->ms;   // tiles of one slice's GEMM launch
+  const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, std::min(active, h->cap), h->sym);
+  const long long t1 = gemm_tiles(tile, h->n, 1, h->sym) * h->ms;   // tiles of one slice's GEMM launch
   const long long slots = 148LL * (tile == TILE_128 ? 1 : (tile == TILE_64 ? 2 : 4));
   const long long launches = (long long)h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
   const long long euler_gemms = (long long)h->mG * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
@@ -516,10 +519,10 @@ static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
 // flow residual of X (device, on rank R's coarse stream) into R.metric[idx]
 static int enqueue_residual(mfode_ctx* h, Rank& R, const double* slab, int count, int idx, int out_idx, double tol,
                             int* flag) {
-  const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, 1);
+  const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, 1, h->sym);
   GemmParams p = base_params(h, 1);
   p.partials = R.partials;
-  const long long ntiles = gemm_tiles(tile, h->n, 1);
+  const long long ntiles = gemm_tiles(tile, h->n, 1, h->sym);
   double denom;
   if (h->flow == MFODE_FLOW_INVERSE) {
     p.shift = 1.0;
@@ -617,6 +620,28 @@ static int load_matrix(mfode_ctx* h, const double* src, bool host, size_t ld_src
   CUDA_TRY(h, cudaStreamSynchronize(st));
   h->normA = R.host_metric[1];
   h->has_result = false;
+  // exact symmetry of A (the symmetric GEMM mode f3 relies on every iterate being a symmetric
+  // polynomial in A); a device input is checked from a host copy
+  {
+    std::vector<double> tmp;
+    const double* hA = src;
+    if (!host) {
+      tmp.resize((size_t)h->n * h->n);
+      CUDA_TRY(h, cudaMemcpy2D(tmp.data(), h->n * sizeof(double), src, ld_src * sizeof(double), h->n * sizeof(double),
+                               h->n, cudaMemcpyDeviceToHost));
+      hA = tmp.data();
+    }
+    const size_t lda = host ? ld_src : (size_t)h->n;
+    bool s = true;
+    for (int i = 0; i < h->n && s; ++i)
+      for (int j = i + 1; j < h->n; ++j)
+        if (hA[(size_t)i * lda + j] != hA[(size_t)j * lda + i]) {
+          s = false;
+          break;
+        }
+    h->a_symmetric = s;
+    if (!s) h->sym = false;
+  }
   return MFODE_OK;
 }
 
@@ -1275,6 +1300,12 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
   if (!h || !key) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!strcmp(key, "overlap")) {
     h->overlap = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "symmetric")) {
+    if (value && !h->a_symmetric) return fail(h, MFODE_EINVAL, "symmetric mode needs A == A^T exactly");
+    if (value && h->small) h->small = false;   // K6 kernels compute full products
+    h->sym = value != 0;
     return MFODE_OK;
   }
   if (!strcmp(key, "pdl")) {   // process-wide: programmatic dependent launch of the GEMMs

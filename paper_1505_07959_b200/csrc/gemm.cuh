@@ -53,6 +53,8 @@ struct GemmParams {
   int b_base, b_step;     // B-operand slice: b_base + (z ^ b_xor) * b_step
   int b_xor;              // 1: pair sub-matrices (trig block flow: X' = A Y, Y' = -A X)
   int alt_sign;           // 1: odd z use -alpha
+  int sym;                // 1: the result is symmetric (all operands polynomials in a symmetric A):
+                          //    compute tiles with tile_m <= tile_n and mirror (f3, half the flops)
   double alpha, beta;     // K = alpha * acc + beta * C
   MatRef C;               // read iff beta != 0
   MatRef X_in, X_out, S, Y_out, F_in, Gold, U_out;
@@ -89,6 +91,21 @@ struct GemmCfg {
 
 __device__ __forceinline__ int rho8(int g) { return ((g & 1) << 2) | (g >> 1); }
 
+// tile index r -> (tile_m, tile_n): row-major, or over the upper triangle tile_m <= tile_n (sym)
+__device__ __forceinline__ void tile_coords(bool sym, int r, int tiles_n, int& tm, int& tn) {
+  if (!sym) {
+    tm = r / tiles_n;
+    tn = r - tm * tiles_n;
+    return;
+  }
+  tm = 0;
+  while (r >= tiles_n - tm) {
+    r -= tiles_n - tm;
+    ++tm;
+  }
+  tn = tm + r;
+}
+
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int EPI>
 __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -106,7 +123,9 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   const int n = p.n;
   const int tiles_m = (n + BM - 1) / BM;
   const int tiles_n = (n + BN - 1) / BN;
-  const int tiles_per_z = tiles_m * tiles_n;
+  // symmetric mode (f3): only tiles with tile_m <= tile_n; the epilogue mirrors them
+  const bool sym = (BM == BN) && p.sym;
+  const int tiles_per_z = sym ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
   const int total = tiles_per_z * p.num_z;
   const int KT = (n + BK - 1) / BK;
 
@@ -142,8 +161,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int z = t / tiles_per_z;
         const int r = t - z * tiles_per_z;
-        const int m0 = (r / tiles_n) * BM;
-        const int n0 = (r % tiles_n) * BN;
+        int tm_, tn_;
+        tile_coords(sym, r, tiles_n, tm_, tn_);
+        const int m0 = tm_ * BM;
+        const int n0 = tn_ * BN;
         const int sa = p.a_base + z * p.a_step;
         const int sb = p.b_base + (z ^ p.b_xor) * p.b_step;
         // Epilogue operands of this tile (X, S, C, F, Gold rows) are prefetched into L2 during the
@@ -200,8 +221,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const int z = t / tiles_per_z;
     const int r = t - z * tiles_per_z;
-    const int m0 = (r / tiles_n) * BM;
-    const int n0 = (r % tiles_n) * BN;
+    int tm_, tn_;
+    tile_coords(sym, r, tiles_n, tm_, tn_);
+    const int m0 = tm_ * BM;
+    const int n0 = tn_ * BN;
     const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
 
     double acc[Cfg::MT][2 * Cfg::NG][2];
@@ -298,9 +321,11 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         } else if constexpr (EPI == EPI_RESID) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
+            // symmetric mode: off-diagonal entries stand for themselves and their mirror
+            const double w = !sym ? 1.0 : ((m0 == n0 && row > col + e) ? 0.0 : (row == col + e ? 1.0 : 2.0));
             if (e < cnt) {
               const double v = k4[e] - ((row == col + e) ? p.shift : 0.0);
-              part = fma(v, v, part);
+              part = fma(w * v, v, part);
             }
           }
         } else {
@@ -377,7 +402,19 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         }
         // ---- stores ----
         auto store4 = [&](double* dst, const double* v) {
-          if (full4) {
+          if (sym) {
+            // upper-triangle tile: write (row, col+e) and its mirror (col+e, row); in a diagonal
+            // tile the strictly-lower elements are written by the mirror of their partner
+            double* base = dst - off;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = col + e;
+              if (e < cnt && !(m0 == n0 && row > cc)) {
+                base[(long long)row * ld + cc] = v[e];
+                if (row != cc) base[(long long)cc * ld + row] = v[e];
+              }
+            }
+          } else if (full4) {
             *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
             *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
           } else {

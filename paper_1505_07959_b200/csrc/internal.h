@@ -41,8 +41,8 @@ cudaError_t launch_lincomb(double* out, const double* Q, long long qstride, cons
 cudaError_t launch_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide,
                             cudaStream_t st);
 cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
-int choose_tile(int n, int num_z);
-long long gemm_tiles(int tile, int n, int num_z);
+int choose_tile(int n, int num_z, bool sym = false);
+long long gemm_tiles(int tile, int n, int num_z, bool sym = false);
 void forget_maps(const double* lo, const double* hi);
 
 constexpr int kFrobPartials = 2 * 296;

@@ -412,14 +412,18 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads, Cfg::kSmemBytes);
     occ = o > 0 ? o : 1;
   });
-  const long long tiles = (long long)((p.n + BM - 1) / BM) * ((p.n + BN - 1) / BN) * p.num_z;
+  const long long tm = (p.n + BM - 1) / BM;
+  const long long tiles = ((BM == BN && p.sym) ? tm * (tm + 1) / 2 : tm * ((p.n + BN - 1) / BN)) * p.num_z;
   // Bounded persistence: a CTA owns at most ~2 ms of tiles.  Kernels are never preempted, so a grid
   // that pinned every SM for a whole (batched, ~100 ms) launch would starve the high-priority coarse
   // stream (the sequential critical path); retiring CTAs every ~2 ms lets its CTAs in.
   const double tile_s = 2.0 * BM * BN * (double)p.n / (37e12 / (num_sms() * occ));
   const long long max_tiles_per_cta = std::max<long long>(1, (long long)(2e-3 / tile_s));
-  long long grid = (long long)num_sms() * occ;
-  grid = std::max(grid, (tiles + max_tiles_per_cta - 1) / max_tiles_per_cta);
+  // The grid is a whole number of waves (a multiple of the resident-CTA slots), so the static
+  // round-robin gives every CTA floor/ceil(tiles / grid) tiles and no wave is left half empty.
+  const long long slots = (long long)num_sms() * occ;
+  const long long waves = std::max<long long>(1, (tiles + slots * max_tiles_per_cta - 1) / (slots * max_tiles_per_cta));
+  long long grid = slots * waves;
   if (grid > tiles) grid = tiles;
   // Programmatic dependent launch: this grid may be scheduled while the previous kernel of the
   // stream drains; the kernel's griddepcontrol.wait orders every global access after it.
@@ -440,17 +444,21 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
 
 int tile_box_rows(int tile) { return tile == TILE_128 ? 128 : (tile == TILE_64 ? 64 : 32); }
 
-int choose_tile(int n, int num_z) {
-  auto tiles = [&](int bm, int bn) { return (long long)((n + bm - 1) / bm) * ((n + bn - 1) / bn) * num_z; };
+int choose_tile(int n, int num_z, bool sym) {
+  auto tiles = [&](int bm, int bn) {
+    const long long tm = (n + bm - 1) / bm;
+    return ((sym && bm == bn) ? tm * (tm + 1) / 2 : tm * ((n + bn - 1) / bn)) * num_z;
+  };
   const int sms = num_sms();
   if (tiles(128, 128) >= 2LL * sms) return TILE_128;
-  if (tiles(64, 64) >= (long long)sms) return TILE_64;
+  if (sym || tiles(64, 64) >= (long long)sms) return TILE_64;   // symmetric mode needs square tiles
   return TILE_32;
 }
 
-long long gemm_tiles(int tile, int n, int num_z) {
+long long gemm_tiles(int tile, int n, int num_z, bool sym) {
   const int bm = tile_box_rows(tile), bn = (tile == TILE_128) ? 128 : 64;
-  return (long long)((n + bm - 1) / bm) * ((n + bn - 1) / bn) * num_z;
+  const long long tm = (n + bm - 1) / bm;
+  return ((sym && bm == bn) ? tm * (tm + 1) / 2 : tm * ((n + bn - 1) / bn)) * num_z;
 }
 
 template <int EPI>
@@ -464,7 +472,7 @@ static cudaError_t dispatch_tile(int tile, const CUtensorMap& ma, const CUtensor
 }
 
 cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st) {
-  if (tile == TILE_AUTO) tile = choose_tile(p.n, p.num_z);
+  if (tile == TILE_AUTO) tile = choose_tile(p.n, p.num_z, p.sym != 0);
   CUtensorMap ma, mb;
   if (!get_map(&ma, A.slab, p.n, p.ld, A.count, tile_box_rows(tile))) return cudaErrorInvalidValue;
   if (!get_map(&mb, B.slab, p.n, p.ld, B.count, 16)) return cudaErrorInvalidValue;

@@ -408,6 +408,45 @@ def test_modified_parareal_vs_oracle(flow, n):
     assert err_gpu <= relF(Xc, seq) + 1e-14
 
 
+@pytest.mark.parametrize("flow,n", [(mf.FLOW_INVERSE, 256), (mf.FLOW_INVERSE, 200), (mf.FLOW_SQRT, 196),
+                                    (mf.FLOW_EXP, 130), (mf.FLOW_TRIG, 100)])
+def test_symmetric_mode_vs_oracle(flow, n):
+    """§8(f) f3(i): with A = A^T every iterate is a symmetric polynomial in A, so each GEMM computes
+    only tiles with tile_m <= tile_n and mirrors them (half the flops).  The result is exactly
+    symmetric and matches the oracle (full products) within the parity bar; the residual
+    reduction counts mirrored entries twice."""
+    if flow == mf.FLOW_SQRT:
+        m = int(round(math.sqrt(n)))
+        A = workloads.laplacian_2d(m) + np.eye(m * m)
+        T, N, mG, mF, K, tol, stop = 20.0, 64, 2, 16, 4, 1e-10, mf.STOP_RESIDUAL
+    else:
+        A = workloads.random_spd(n, 20).A
+        T, N, mG, mF, K, tol, stop = 1.0, 6, 1, 8, 6, 1e-11, mf.STOP_DELTA
+    s = mf.Solver(A, flow, T, N, mG, mF)
+    s.set_option("symmetric", 1)
+    info = s.solve(K, tol, stop)
+    rows = 2 * n if flow == mf.FLOW_TRIG else n
+    X = np.empty((rows, n))
+    s.result(X)
+    ref = dense.solve(A, flow, T, N, mG, mF, K, tol, stop)
+    assert info["k_done"] == ref["k_done"]
+    assert relF(X, ref["X"]) <= 1e-10
+    for b in range(rows // n):
+        blk = X[b * n:(b + 1) * n]
+        assert np.array_equal(blk, blk.T)
+    if flow in (mf.FLOW_INVERSE, mf.FLOW_SQRT):
+        r_sym = s.residual()
+        r_ref = dense.flow_residual(A, flow)(X)
+        assert abs(r_sym - r_ref) <= 1e-6 * r_ref + 1e-15
+
+
+def test_symmetric_mode_rejects_nonsymmetric():
+    A = workloads.random_nonsymmetric(80, 2)
+    s = mf.Solver(A, mf.FLOW_INVERSE, 1.0, 4, 1, 4)
+    with pytest.raises(mf.MfodeError):
+        s.set_option("symmetric", 1)
+
+
 def test_small_kernels_logical_ranks_and_sequential():
     w = workloads.config(0)
     s1, i1, X1 = _solve_gpu(w.A, w.flow, w.T, w.N, w.m_G, w.m_F, 8, 1e-13, mf.STOP_DELTA)
