@@ -98,7 +98,8 @@ typedef struct {
   int gpu_launches;    /* kernels launched by the solve (all logical ranks of this process)      */
   int fine_kernel_launches;  /* fine-propagator GEMM launches of the used sweeps (this process)  */
   double fine_kernel_ms;     /* summed CUDA-event duration of those launches (fine stream)       */
-  double fine_kernel_flops;  /* algorithmic flops of those launches                              */
+  double fine_kernel_flops;  /* flops those launches executed (algorithmic; in the symmetric
+                                mode only the upper-triangle tiles, i.e. ~half)                  */
   double deltas[64];   /* delta of sweep k+1 in deltas[k] (first 64 sweeps)                     */
 } mfode_solve_info;
 

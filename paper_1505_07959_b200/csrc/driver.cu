@@ -425,6 +425,10 @@ static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
     ct.iter = k;
     ct.launches = h->small ? 1 : h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
     ct.flops = (double)(jb - ja) * h->mF * rk4_flops(h);
+    if (h->sym && !h->small) {   // executed (not algorithmic) flops: only upper-triangle tiles run
+      const int tl = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, (jb - ja) * h->ms, true);
+      ct.flops *= (double)gemm_tiles(tl, h->n, 1, true) / (double)gemm_tiles(tl, h->n, 1, false);
+    }
     CUDA_TRY(h, cudaEventRecord(ct.t0, R.fine));
     TRY(fine_chunk(h, R, par, ja, jb, flag));
     CUDA_TRY(h, cudaEventRecord(ct.t1, R.fine));
