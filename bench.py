@@ -138,6 +138,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sym-steps", type=int, default=1, help="timed solves of the f3 symmetric variant (0: skip)")
+    ap.add_argument("--emu-steps", type=int, default=1,
+                    help="timed solves of the f3(ii) int8-tensor-core emulated variant (0: skip)")
+    ap.add_argument("--emu-moduli", type=int, default=16)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -244,34 +247,51 @@ def main():
     e2e_value = e2e_flops / (e2e_ms * 1e-3) / 1e12 if args.e2e_steps > 0 else None
     resid = solver.residual()
 
-    # f3(i) symmetric variant, reported beside (never folded into) value: A = A^T, so every GEMM
-    # computes only its upper-triangle tiles and mirrors them (half the executed flops).
-    sym = None
-    if args.sym_steps > 0:
+    def variant(opts, steps):
+        """Time `steps` solves with solver options `opts` (reported beside, never folded into, value)."""
         try:
-            solver.set_option("symmetric", 1)
+            for k, v in opts.items():
+                solver.set_option(k, v)
             solver.solve(w.K_max, w.tol, w.stop)      # warm-up
             barrier()
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record()
-            sinfos = [solver.solve(w.K_max, w.tol, w.stop) for _ in range(args.sym_steps)]
+            vinfos = [solver.solve(w.K_max, w.tol, w.stop) for _ in range(steps)]
             s1.record()
             s1.synchronize()
-            sms = s0.elapsed_time(s1) / args.sym_steps
+            vms = s0.elapsed_time(s1) / steps
             if world > 1:
-                t = torch.tensor([sms], dtype=torch.float64, device="cuda")
+                t = torch.tensor([vms], dtype=torch.float64, device="cuda")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                sms = float(t.item())
-            sres = solver.residual()
-            solver.set_option("symmetric", 0)
-            ffl = float(np.mean([i["fine_flops"] for i in sinfos]))
-            sym = {"time_to_tol_ms": sms, "k_done": sinfos[-1]["k_done"], "residual": sres,
-                   "algorithmic_fine_tflops": ffl / (sms * 1e-3) / 1e12,
-                   "executed_fine_tflops_approx": ffl * (w.n // 128 + 1) / (2 * (w.n // 128)) / (sms * 1e-3) / 1e12,
-                   "speedup_vs_full": ms_step / sms}
+                vms = float(t.item())
+            vres = solver.residual()
+            X_v = np.empty((w.n, w.n))
+            solver.result(X_v)
+            for k in opts:
+                solver.set_option(k, 0)
+            ffl = float(np.mean([i["fine_flops"] for i in vinfos]))
+            vkms = sum(i["fine_kernel_ms"] for i in vinfos)
+            vkfl = sum(i["fine_kernel_flops"] for i in vinfos)
+            return {"options": opts, "time_to_tol_ms": vms, "k_done": vinfos[-1]["k_done"], "residual": vres,
+                    "algorithmic_fine_tflops": ffl / (vms * 1e-3) / 1e12,
+                    "fine_phase_tflops_algorithmic": (vkfl / (vkms * 1e-3) / 1e12) if vkms > 0 else None,
+                    "speedup_vs_full": ms_step / vms,
+                    "rel_frob_diff_vs_dmma_result": float(np.linalg.norm(X_v - X_host) / np.linalg.norm(X_host)),
+                    "gpu_launches": int(sum(i["gpu_launches"] for i in vinfos))}
         except Exception as e:   # noqa: BLE001
-            sym = {"error": str(e)}
+            return {"options": opts, "error": str(e)}
+
+    # f3(i) symmetric variant: A = A^T, so every GEMM computes only its upper-triangle tiles and
+    # mirrors them (half the executed flops).
+    sym = variant({"symmetric": 1}, args.sym_steps) if args.sym_steps > 0 else None
+    if sym and "time_to_tol_ms" in sym:
+        sym["executed_fine_tflops_approx"] = (sym["algorithmic_fine_tflops"] * (w.n // 128 + 1) / (2 * (w.n // 128)))
+    # f3(ii) every GEMM (except the residual's) emulated on the int8 tensor cores (CRT/Ozaki-II, exact
+    # integer products of 55-bit-scaled operands), alone and combined with f3(i)
+    emu = variant({"emulation": args.emu_moduli}, args.emu_steps) if args.emu_steps > 0 else None
+    emu_sym = (variant({"emulation": args.emu_moduli, "symmetric": 1}, args.emu_steps)
+               if args.emu_steps > 0 else None)
 
     if rank == 0:
         cpu = None
@@ -305,6 +325,8 @@ def main():
                          "cublas_dgemm_4096_tflops": cublas},
             "cpu_baseline": cpu,
             "f3_symmetric_variant": sym,
+            "f3_emulated_variant": emu,
+            "f3_emulated_symmetric_variant": emu_sym,
         }
         print(json.dumps(line), flush=True)
     solver.close()

@@ -163,7 +163,10 @@ MFODE_API int mfode_get_slice(mfode_ctx *h, int n_index, double *U);
 /* Tuning knobs (all optional).  key: "fine_batch" (max slices per batched fine launch; 0 = auto),
  * "overlap" (1 = speculative next-iteration fine work overlapped with the correction sweep,
  * 0 = strictly phased), "tile" (0 = auto, 1 = 128x128, 2 = 64x64, 3 = 32x64 GEMM tiles), "small" (1 = K6
- * shared-memory persistent kernels, default for n <= 64; 0 = one launch per GEMM). */
+ * shared-memory persistent kernels, default for n <= 64; 0 = one launch per GEMM), "symmetric" (1 = f3(i)
+ * half-flop symmetric GEMMs, needs A == A^T bitwise), "emulation" (f3(ii): 0 = FP64 DMMA GEMMs;
+ * 8..16 = every GEMM except the residual's emulated on the int8 tensor cores with that many CRT
+ * moduli, see mfode_dgemm_emulated; EINVAL if n leaves fewer than 8 bits per operand). */
 MFODE_API int mfode_set_option(mfode_ctx *h, const char *key, int64_t value);
 
 MFODE_API const char *mfode_last_error(const mfode_ctx *h);
@@ -199,6 +202,24 @@ MFODE_API int mfode_accel_inverse(const double *A, const double *X0, const doubl
  * mfode_set_option.  Errors: EINVAL, ECUDA. */
 MFODE_API int mfode_dgemm(const double *dA, const double *dB, const double *dC, double *dD, int64_t n,
                 int64_t ld, double alpha, double beta, int tile, void *cuda_stream);
+
+/* f3(ii): the same product D = alpha * A_op * B_op + beta * C computed on the int8
+ * tensor cores (tcgen05.mma kind::i8, TMEM accumulators) by CRT ("Ozaki scheme II") emulation:
+ * row i of A_op and column j of B_op are scaled by powers of two and rounded to integers of
+ * a + 1 bits (a = floor((log2 M - 2 - ceil(log2 n)) / 2), M = product of the first n_moduli of
+ * {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193}: a = 55 for 16
+ * moduli at n = 4096); the integer product is formed EXACTLY from n_moduli int8 GEMMs (one per
+ * modulus) and the Chinese remainder theorem, then scaled back with one correctly rounded
+ * conversion.  Error per element <= 2^-(a+1) (2^e_i sum_k |B_kj| + 2^f_j sum_k |A_ik|) + rounding,
+ * where 2^e_i > max_k |A_ik|, 2^f_j > max_k |B_kj|.  Deterministic (bitwise reproducible).
+ * n_moduli in 2..16.  Same buffers / layout / stream semantics as mfode_dgemm.  Scratch
+ * (3 n_moduli n^2 bytes + O(n)) is cached per stream until mfode_release_workspace(stream).
+ * Errors: EINVAL, ECUDA, ENOMEM. */
+MFODE_API int mfode_dgemm_emulated(const double *dA, const double *dB, const double *dC, double *dD, int64_t n,
+                                   int64_t ld, double alpha, double beta, int n_moduli, void *cuda_stream);
+
+/* Free the emulation scratch cached for cuda_stream (synchronises the stream). */
+MFODE_API int mfode_release_workspace(void *cuda_stream);
 
 /* One fused RK4 stage on device buffers (the fine propagator's second GEMM with its stage
  * epilogue): K = alpha*Yop*Bop + beta*C, then for stage s (1..4) with step h:

@@ -37,7 +37,7 @@ EXPORTED = [
     "mfode_residual", "mfode_get_result", "mfode_get_result_device", "mfode_get_slice", "mfode_set_option",
     "mfode_last_error", "mfode_destroy", "mfode_dgemm", "mfode_rk_stage", "mfode_frobenius", "mfode_partition",
     "mfode_kernel_launches", "mfode_last_global_error", "mfode_version", "mfode_cosine", "mfode_accel_inverse",
-    "mfode_modified_parareal_solve",
+    "mfode_modified_parareal_solve", "mfode_dgemm_emulated", "mfode_release_workspace",
 ]
 
 
@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
         "mfode_last_error": (ctypes.c_char_p, [P]),
         "mfode_destroy": (None, [P]),
         "mfode_dgemm": (I, [P, P, P, P, I64, I64, D, D, I, P]),
+        "mfode_dgemm_emulated": (I, [P, P, P, P, I64, I64, D, D, I, P]),
+        "mfode_release_workspace": (I, [P]),
         "mfode_rk_stage": (I, [P, P, P, D, D, P, P, P, I, D, I64, I64, I, P]),
         "mfode_frobenius": (I, [P, P, I64, I64, ctypes.POINTER(D), P]),
         "mfode_partition": (I, [I, I, I, ctypes.POINTER(I), ctypes.POINTER(I)]),
@@ -254,6 +256,25 @@ def dgemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, tile: i
     _check(lib().mfode_dgemm(_ptr(A), _ptr(B), _ptr(C), _ptr(out), n, ld, alpha, beta, tile,
                              _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
     return out
+
+
+def dgemm_emulated(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, n_moduli: int = 16,
+                   stream=None):
+    """D = alpha A B + beta C emulated on the int8 tensor cores (mfode_dgemm_emulated, f3(ii))."""
+    import torch
+    n = A.shape[0]
+    ld = A.stride(0)
+    if out is None:
+        out = torch.empty_strided(A.shape, A.stride(), dtype=A.dtype, device=A.device)
+    _check(lib().mfode_dgemm_emulated(_ptr(A), _ptr(B), _ptr(C), _ptr(out), n, ld, alpha, beta, n_moduli,
+                                      _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
+    return out
+
+
+def release_workspace(stream=None):
+    """Free the emulated-GEMM scratch cached for `stream` (mfode_release_workspace)."""
+    import torch
+    _check(lib().mfode_release_workspace(_stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
 
 
 def rk_stage(Yop, Bop, X, S, Ynext, stage: int, h: float, C=None, alpha: float = 1.0, beta: float = 0.0,

@@ -128,6 +128,7 @@ struct mfode_ctx {
   int tile = 0;              // 0 auto
   bool small = false;        // K6 shared-memory kernels (n <= kSmallMaxN)
   bool sym = false;          // f3: symmetric GEMMs (upper tiles + mirror), needs A == A^T exactly
+  int oz_nmod = 0;           // f3(ii): > 0 = GEMMs emulated on the int8 tensor cores with this many moduli
   bool a_symmetric = false;  // A == A^T bitwise (checked at load)
   bool overlap = true;
   int fine_batch_opt = 0;
@@ -223,6 +224,7 @@ static GemmParams base_params(const mfode_ctx* h, int num_z) {
   p.alpha = 1.0;
   p.beta = 0.0;
   p.sym = h->sym ? 1 : 0;
+  p.oz_nmod = h->oz_nmod;
   return p;
 }
 
@@ -600,8 +602,16 @@ static void free_rank(mfode_ctx* h, Rank& R) {
       cudaFree(b);
     }
   if (R.host_metric) cudaFreeHost(R.host_metric);
-  if (R.fine) cudaStreamDestroy(R.fine);
-  if (R.coarse) cudaStreamDestroy(R.coarse);
+  if (R.fine) {
+    cudaStreamSynchronize(R.fine);
+    oz_release(R.fine);
+    cudaStreamDestroy(R.fine);
+  }
+  if (R.coarse) {
+    cudaStreamSynchronize(R.coarse);
+    oz_release(R.coarse);
+    cudaStreamDestroy(R.coarse);
+  }
   for (auto e : R.evC) cudaEventDestroy(e);
   for (auto e : R.evF) cudaEventDestroy(e);
   for (auto& ct : R.tpool) {
@@ -1312,6 +1322,28 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     h->sym = value != 0;
     return MFODE_OK;
   }
+  if (!strcmp(key, "emulation")) {
+    // f3(ii): FP64 GEMMs emulated on the int8 tensor cores (ozaki.cu) with `value` moduli; 0 = DMMA
+    if (value != 0 && (value < 8 || value > kOzMaxModuli))
+      return fail(h, MFODE_EINVAL, "emulation needs 0 (off) or 8..%d moduli", kOzMaxModuli);
+    OzConst c;
+    if (value != 0 && !oz_make_const((int)value, h->n, &c))
+      return fail(h, MFODE_EINVAL, "n = %d too large for %lld moduli", h->n, (long long)value);
+    if (value && h->small) h->small = false;   // K6 kernels do not go through the GEMM dispatch
+    h->oz_nmod = (int)value;
+    if (value) {
+      CUDA_TRY(h, cudaSetDevice(h->device));
+      for (auto& R : h->ranks) {
+        CUDA_TRY(h, oz_reserve(R.fine, h->n, h->cap * h->ms, (int)value));
+        CUDA_TRY(h, oz_reserve(R.coarse, h->n, h->ms, (int)value));
+      }
+    }
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "oz_pair")) {   // process-wide: CTA-pair (1, default) or single-CTA (0) int8 GEMM kernel
+    g_oz_pair = value != 0;
+    return MFODE_OK;
+  }
   if (!strcmp(key, "pdl")) {   // process-wide: programmatic dependent launch of the GEMMs
     g_pdl = value != 0;
     return MFODE_OK;
@@ -1387,6 +1419,36 @@ int mfode_dgemm(const double* dA, const double* dB, const double* dC, double* dD
   Operand A{dA, 1, 0, 0}, B{dB, 1, 0, 0};
   cudaError_t e = launch_gemm(EPI_STORE, tile, A, B, p, (cudaStream_t)stream);
   if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "dgemm: %s", cudaGetErrorString(e));
+  return MFODE_OK;
+}
+
+int mfode_dgemm_emulated(const double* dA, const double* dB, const double* dC, double* dD, int64_t n, int64_t ld,
+                         double alpha, double beta, int n_moduli, void* stream) {
+  if (!dA || !dB || !dD || (beta != 0.0 && !dC)) return set_global_err(MFODE_EINVAL, "NULL argument");
+  if (n < 1 || ld < n || (ld * 8) % 16 != 0) return set_global_err(MFODE_EINVAL, "bad n/ld");
+  OzConst c;
+  if (n_moduli < 2 || n_moduli > kOzMaxModuli || !oz_make_const(n_moduli, (int)n, &c))
+    return set_global_err(MFODE_EINVAL, "n_moduli must be 2..%d and leave >= 8 bits per operand", kOzMaxModuli);
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = (int)n;
+  p.ld = (int)ld;
+  p.num_z = 1;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.C = MatRef{const_cast<double*>(dC), 0};
+  p.Y_out = MatRef{dD, 0};
+  p.oz_nmod = n_moduli;
+  Operand A{dA, 1, 0, 0}, B{dB, 1, 0, 0};
+  cudaError_t e = launch_gemm(EPI_STORE, TILE_AUTO, A, B, p, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "dgemm_emulated: %s", cudaGetErrorString(e));
+  return MFODE_OK;
+}
+
+int mfode_release_workspace(void* stream) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  oz_release((cudaStream_t)stream);
+  if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "release_workspace: %s", cudaGetErrorString(e));
   return MFODE_OK;
 }
 

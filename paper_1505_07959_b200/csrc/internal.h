@@ -41,6 +41,26 @@ cudaError_t launch_lincomb(double* out, const double* Q, long long qstride, cons
 cudaError_t launch_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide,
                             cudaStream_t st);
 cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
+
+// f3(ii): FP64 GEMM emulated on the int8 tensor cores (ozaki.cu).  launch_gemm routes here when
+// p.oz_nmod > 0 (every epilogue except EPI_RESID).  Workspaces are per stream.
+constexpr int kOzMaxModuli = 16;
+struct OzConst {
+  int nmod;
+  int abits;                           // operands are scaled to integers of magnitude <= 2^abits
+  uint32_t m[kOzMaxModuli];            // moduli
+  double minv[kOzMaxModuli];           // 1 / m
+  unsigned long long wlo[kOzMaxModuli], whi[kOzMaxModuli];   // CRT weights w_t (128-bit)
+  double wf[kOzMaxModuli];             // w_t / M
+  unsigned long long Mlo, Mhi;         // M = prod m_t (128-bit)
+  uint32_t pw[kOzMaxModuli / 2][4];    // CRT weights of the pair groups (m_2i m_2i+1), 32-bit limbs
+  double pwf[kOzMaxModuli / 2];        // pair weight / M
+};
+bool oz_make_const(int nmod, int k, OzConst* c);
+cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
+cudaError_t oz_reserve(cudaStream_t st, int n, int max_z, int nmod);
+void oz_release(cudaStream_t st);
+extern bool g_oz_pair;   // option "oz_pair" (process-wide)
 int choose_tile(int n, int num_z, bool sym = false);
 long long gemm_tiles(int tile, int n, int num_z, bool sym = false);
 void forget_maps(const double* lo, const double* hi);

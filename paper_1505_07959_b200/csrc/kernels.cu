@@ -472,6 +472,7 @@ static cudaError_t dispatch_tile(int tile, const CUtensorMap& ma, const CUtensor
 }
 
 cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st) {
+  if (p.oz_nmod > 0 && epi != EPI_RESID) return launch_gemm_oz(epi, A, B, p, st);
   if (tile == TILE_AUTO) tile = choose_tile(p.n, p.num_z, p.sym != 0);
   CUtensorMap ma, mb;
   if (!get_map(&ma, A.slab, p.n, p.ld, A.count, tile_box_rows(tile))) return cudaErrorInvalidValue;

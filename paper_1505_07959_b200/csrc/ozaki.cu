@@ -1,0 +1,913 @@
+// Emulated FP64 GEMM on the int8 tensor cores (tcgen05 kind::i8, TMEM accumulators) -- SURVEY.md
+// §8(f) f3(ii).  B200's FP64 tensor path (DMMA, 37 TF/s measured) is ~1/120 of its int8 tensor peak,
+// so the dense n x n FP64 products of the fine propagator (P:44 RK stages, north star) can be
+// computed faster, to FP64-level accuracy, as a handful of EXACT integer GEMMs:
+//
+//   1. scale (encode): every row i of the left operand A is scaled by 2^(a - e_i) (e_i = exponent
+//      of the row's max |A_ik|) and rounded to an integer A'_ik, |A'_ik| <= 2^a; every column j of
+//      the right operand B likewise to B'_kj, |B'_kj| <= 2^a.  C' = A' B' is an integer matrix with
+//      |C'_ij| <= k 2^(2a) < M/4, M = m_1 ... m_T (T pairwise-coprime moduli <= 256).
+//   2. for each modulus m_t: the residues (A' mod m_t), (B' mod m_t) fit int8 (symmetric range),
+//      so C'_t = (A' mod m_t)(B' mod m_t) is an exact int32 GEMM on the tensor cores
+//      (|sum| <= k * 128^2 < 2^31 for k < 2^17); its epilogue stores C'_t mod m_t as one byte.
+//   3. decode: C' is recovered EXACTLY from its residues by the Chinese remainder theorem
+//      (C' = sum_t r_t w_t mod M, 128-bit integer arithmetic), converted to double with one
+//      correctly-rounded conversion and scaled back by 2^(e_i + f_j - 2a); the fused parareal
+//      epilogue of the DMMA path (epilogue.cuh) then runs on it unchanged.
+// This is the CRT ("Ozaki scheme II") form of integer-tensor-core FP64 emulation.  The only error
+// is the rounding of the inputs to a+1 significant bits relative to their row (column) maximum
+// (a = 55 for T = 16 moduli at k = 4096, vs 53 bits of an FP64 significand) plus the final
+// rounding; every step is deterministic integer arithmetic, so results are bitwise reproducible
+// and independent of batch, tile order, rank count and stream timing (prefix exactness and
+// P-invariance hold as on the DMMA path).
+//
+// Kernels: k_oz_enc_rows (left operand, row-scaled, K-major int8 planes), k_oz_colexp +
+// k_oz_enc_colsT (right operand, column-scaled, transposed to K-major planes), oz_gemm_kernel
+// (persistent, warp-specialised: TMA producer warp, single-thread tcgen05.mma issuer, 4 epilogue
+// warps reading the double-buffered TMEM accumulators), k_oz_decode<EPI> (CRT + fused epilogue).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "gemm.cuh"
+#include "internal.h"
+
+namespace mfode {
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+// Pairwise-coprime moduli (256 = 2^8, 255 = 3*5*17, 253 = 11*23, 247 = 13*19, 217 = 7*31, others prime).
+static const uint32_t kOzModuli[kOzMaxModuli] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                                 229, 227, 223, 217, 211, 199, 197, 193};
+
+static uint32_t modinv_small(uint32_t a, uint32_t m) {   // a^-1 mod m, gcd(a, m) = 1
+  long long t = 0, nt = 1, r = m, nr = a % m;
+  while (nr) {
+    const long long q = r / nr;
+    long long tmp = t - q * nt; t = nt; nt = tmp;
+    tmp = r - q * nr; r = nr; nr = tmp;
+  }
+  if (t < 0) t += m;
+  return (uint32_t)t;
+}
+
+bool oz_make_const(int nmod, int k, OzConst* c) {
+  if (nmod < 2 || nmod > kOzMaxModuli || k < 1) return false;
+  memset(c, 0, sizeof(*c));
+  c->nmod = nmod;
+  u128 M = 1;
+  double log2M = 0.0;
+  for (int t = 0; t < nmod; ++t) {
+    M *= kOzModuli[t];
+    log2M += std::log2((double)kOzModuli[t]);
+  }
+  int kbits = 0;
+  while ((1LL << kbits) < k) ++kbits;
+  // |C'| <= k 2^(2a) must stay below M/4 (the CRT rounding margin)
+  c->abits = (int)std::floor((log2M - 2.0 - kbits) / 2.0 - 1e-9);
+  if (c->abits > 60) c->abits = 60;   // the encoder's 20-bit limb split keeps |x| < 2^61
+  if (c->abits < 8) return false;
+  c->Mlo = (unsigned long long)M;
+  c->Mhi = (unsigned long long)(M >> 64);
+  for (int t = 0; t < nmod; ++t) {
+    const uint32_t m = kOzModuli[t];
+    const u128 Mt = M / m;
+    const uint32_t inv = modinv_small((uint32_t)(Mt % m), m);
+    const u128 w = Mt * inv;   // < M: w = 1 mod m_t, 0 mod the others
+    c->m[t] = m;
+    c->minv[t] = 1.0 / (double)m;
+    c->wlo[t] = (unsigned long long)w;
+    c->whi[t] = (unsigned long long)(w >> 64);
+    c->wf[t] = (double)((long double)w / (long double)M);
+  }
+  // the decode combines residues in pairs (m_2i, m_2i+1) first; a lone last modulus forms its own group
+  for (int i = 0; 2 * i < nmod; ++i) {
+    const uint32_t P = kOzModuli[2 * i] * (2 * i + 1 < nmod ? kOzModuli[2 * i + 1] : 1u);
+    const u128 Mi = M / P;
+    const uint32_t inv = modinv_small((uint32_t)(Mi % P), P);
+    const u128 w = Mi * inv;
+    for (int j = 0; j < 4; ++j) c->pw[i][j] = (uint32_t)(w >> (32 * j));
+    c->pwf[i] = (double)((long double)w / (long double)M);
+  }
+  return true;
+}
+
+// CRT constants for every moduli count (index nmod), in constant memory: the kernels index them with
+// a runtime modulus number (uniform across the warp), which kernel parameters cannot do without a
+// local-memory copy.  Filled once per device; abits (which also depends on k) travels as a parameter.
+__constant__ OzConst c_oz[kOzMaxModuli + 1];
+
+static cudaError_t oz_init_device() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && done[dev]) return cudaSuccess;
+  OzConst tab[kOzMaxModuli + 1];
+  memset(tab, 0, sizeof(tab));
+  for (int t = 2; t <= kOzMaxModuli; ++t) oz_make_const(t, 1, &tab[t]);
+  cudaError_t e = cudaMemcpyToSymbol(c_oz, tab, sizeof(tab));
+  if (e == cudaSuccess && dev < 64) done[dev] = true;
+  return e;
+}
+
+// ---------------------------------------------------------------------------------------------
+// encode
+// ---------------------------------------------------------------------------------------------
+// Residue of the scaled integer x (|x| <= 2^60) modulo the compile-time modulus M, symmetric range:
+// x = x2 2^40 + x1 2^20 + x0 (x0, x1 in [0, 2^20)), x mod M = (x2 c2 + x1 c1 + x0) mod M with
+// c1 = 2^20 mod M, c2 = 2^40 mod M; |x2 c2 + x1 c1 + x0| < 2^29, so 32-bit integer arithmetic with a
+// constant divisor (multiply-high) is exact.
+template <uint32_t M>
+__device__ __forceinline__ int oz_res(int x0, int x1, int x2) {
+  constexpr int c1 = (int)((1ull << 20) % M), c2 = (int)((1ull << 40) % M);
+  const int s = x2 * c2 + x1 * c1 + x0;
+  int r = s % (int)M;
+  if (r < 0) r += (int)M;
+  if (2 * r >= (int)M) r -= (int)M;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+  return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) | ((uint32_t)(d & 255) << 24);
+}
+
+// Writes the residues of 4 consecutive scaled integers to planes t = 0..nmod-1 (plane stride pstride).
+__device__ __forceinline__ void oz_write_residues4(int8_t* dst, long long pstride, const long long (&x)[4], int nmod) {
+  int l0[4], l1[4], l2[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    l0[q] = (int)(x[q] & 0xFFFFF);
+    l1[q] = (int)((x[q] >> 20) & 0xFFFFF);
+    l2[q] = (int)(x[q] >> 40);
+  }
+#define OZ_PLANE(T, MV)                                                                                 \
+  if (T < nmod)                                                                                       \
+    *reinterpret_cast<uint32_t*>(dst + (T) * pstride) =                                               \
+        pack4(oz_res<MV>(l0[0], l1[0], l2[0]), oz_res<MV>(l0[1], l1[1], l2[1]), oz_res<MV>(l0[2], l1[2], l2[2]), \
+              oz_res<MV>(l0[3], l1[3], l2[3]));
+  OZ_PLANE(0, 256) OZ_PLANE(1, 255) OZ_PLANE(2, 253) OZ_PLANE(3, 251) OZ_PLANE(4, 247) OZ_PLANE(5, 241)
+  OZ_PLANE(6, 239) OZ_PLANE(7, 233) OZ_PLANE(8, 229) OZ_PLANE(9, 227) OZ_PLANE(10, 223) OZ_PLANE(11, 217)
+  OZ_PLANE(12, 211) OZ_PLANE(13, 199) OZ_PLANE(14, 197) OZ_PLANE(15, 193)
+#undef OZ_PLANE
+}
+
+__device__ __forceinline__ int exp_of_max(double mx) {   // smallest e with mx < 2^e (mx > 0)
+  int e;
+  frexp(mx, &e);
+  return e;
+}
+
+constexpr int kEncThreads = 128;
+
+// Left operand: row i of matrix (base + z*step) -> nmod int8 planes [z*nmod + t][i][0..ld_k), K-major.
+__global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab, long long mstride, int base, int step,
+                                                              int n, int ld, int8_t* planes, long long pstride,
+                                                              int ldk, double* rscale, int nmod, int abits, const int* flag) {
+  if (flag != nullptr && *(volatile const int*)flag != 0) return;
+  const int row = blockIdx.x, z = blockIdx.y;
+  const double* src = slab + (long long)(base + z * step) * mstride + (long long)row * ld;
+  __shared__ double red[kEncThreads / 32];
+  __shared__ int bad_s;
+  if (threadIdx.x == 0) bad_s = 0;
+  __syncthreads();
+  double mx = 0.0;
+  bool bad = false;
+  for (int k = 4 * threadIdx.x; k < n; k += 4 * kEncThreads) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (k + e < n) {
+        const double v = fabs(src[k + e]);
+        bad |= !(v <= 1.7976931348623157e308);
+        mx = fmax(mx, v);
+      }
+  }
+  if (bad) bad_s = 1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int w = 1; w < kEncThreads / 32; ++w) mx = fmax(mx, red[w]);
+  const int e = (mx > 0.0) ? exp_of_max(mx) : 0;
+  const double scale = ldexp(1.0, abits - e);
+  if (threadIdx.x == 0) rscale[(long long)z * n + row] = bad_s ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, e - abits);
+  int8_t* dst = planes + (long long)z * nmod * pstride + (long long)row * ldk;
+  for (int k = 4 * threadIdx.x; k < ldk; k += 4 * kEncThreads) {
+    long long x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = (k + q < n && !bad_s) ? __double2ll_rn(src[k + q] * scale) : 0LL;
+    oz_write_residues4(dst + k, pstride, x, nmod);
+  }
+}
+
+// Right operand, pass 1: colexp[z][j] = max over rows of the exponent of |B_kj| (atomicMax over
+// row chunks; kOzBad for a non-finite column).  colexp is preset to a very negative value.
+constexpr int kOzBad = 1 << 30;
+__global__ void k_oz_colexp(const double* slab, long long mstride, int base, int step, int n, int ld, int* colexp,
+                            const int* flag) {
+  if (flag != nullptr && *(volatile const int*)flag != 0) return;
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int z = blockIdx.z;
+  const int r0 = blockIdx.y * 256;
+  if (j >= n) return;
+  const double* src = slab + (long long)(base + z * step) * mstride + j;
+  double mx = 0.0;
+  bool bad = false;
+  for (int r = r0 + (threadIdx.x >> 5); r < n && r < r0 + 256; r += blockDim.x >> 5) {
+    const double v = fabs(src[(long long)r * ld]);
+    bad |= !(v <= 1.7976931348623157e308);
+    mx = fmax(mx, v);
+  }
+  const int e = bad ? kOzBad : (mx > 0.0 ? exp_of_max(mx) : -kOzBad);
+  atomicMax(&colexp[(long long)z * n + j], e);
+}
+
+// Right operand, pass 2: B'[k][j] -> planes [z*nmod + t][j][k] (transposed: K-major for the MMA).
+constexpr int kTT = 64;   // 64 x 64 transpose tile
+__global__ void __launch_bounds__(256) k_oz_enc_colsT(const double* slab, long long mstride, int base, int step,
+                                                       int n, int ld, const int* colexp, int8_t* planes,
+                                                       long long pstride, int ldk, double* cscale, int nmod,
+                                                       int abits, const int* flag) {
+  if (flag != nullptr && *(volatile const int*)flag != 0) return;
+  __shared__ double tile[kTT][kTT + 1];
+  const int j0 = blockIdx.x * kTT, k0 = blockIdx.y * kTT, z = blockIdx.z;
+  const double* src = slab + (long long)(base + z * step) * mstride;
+  for (int idx = threadIdx.x; idx < kTT * kTT; idx += 256) {
+    const int kk = idx / kTT, jj = idx % kTT;
+    tile[kk][jj] = (k0 + kk < n && j0 + jj < n) ? src[(long long)(k0 + kk) * ld + j0 + jj] : 0.0;
+  }
+  __syncthreads();
+  int8_t* dst = planes + (long long)z * nmod * pstride;
+  for (int w = threadIdx.x; w < kTT * (kTT / 4); w += 256) {
+    const int jj = w / (kTT / 4), kq = w % (kTT / 4);
+    const int j = j0 + jj, k = k0 + 4 * kq;
+    if (j >= n || k >= ldk) continue;
+    const int e = colexp[(long long)z * n + j];
+    const bool bad = (e == kOzBad);
+    const int ee = (e <= -kOzBad) ? 0 : e;
+    if (blockIdx.y == 0 && kq == 0)
+      cscale[(long long)z * n + j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, ee - abits);
+    const double scale = ldexp(1.0, abits - ee);
+    long long x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = bad ? 0LL : __double2ll_rn(tile[4 * kq + q][jj] * scale);
+    oz_write_residues4(dst + (long long)j * ldk + k, pstride, x, nmod);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// int8 tensor-core GEMM, one modulus per plane: R_t = (A_t B_t^T) mod m_t  (bytes)
+// ---------------------------------------------------------------------------------------------
+constexpr int OZ_BM = 128, OZ_BN = 256, OZ_BK = 128, OZ_ST = 4;
+constexpr int OZ_A_BYTES = OZ_BM * OZ_BK, OZ_B_BYTES = OZ_BN * OZ_BK, OZ_STAGE = OZ_A_BYTES + OZ_B_BYTES;
+constexpr int OZ_THREADS = 192;   // warp 0: TMA, warp 1: TMEM alloc + MMA issue, warps 2-5: epilogue
+constexpr int OZ_SMEM = OZ_ST * OZ_STAGE + 1024 + 256;
+constexpr uint32_t OZ_TMEM_COLS = 2 * OZ_BN;   // double-buffered int32 accumulators
+
+struct OzGemmArgs {
+  int n, num_z, nmod;
+  int a_step, b_step, b_xor;
+  int sym;               // only tiles meeting the upper triangle (row <= col) are computed
+  uint8_t* R;
+  long long rpstride;
+  int ldr;
+  const int* flag;
+};
+
+__device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, int t, int tiles_m, int tiles_n, int& plane, int& m0,
+                                        int& n0) {
+  const int per = tiles_m * tiles_n;
+  plane = t / per;
+  const int r = t - plane * per;
+  const int tm = r / tiles_n;
+  m0 = tm * OZ_BM;
+  n0 = (r - tm * tiles_n) * OZ_BN;
+  return !(g.sym && m0 > n0 + OZ_BN - 1);   // entirely below the diagonal: skipped in symmetric mode
+}
+
+// Epilogue of one accumulator tile row slice: 256 int32 columns of TMEM (this warp's lane quadrant,
+// starting at column address taddr) -> residues mod m (bytes) at dst[n0 ..), row `row`.
+// |x| <= k 128^2 <= 2^30 (k <= 2^16), so u = x + m 2^23 is a non-negative 32-bit integer congruent
+// to x, and u mod m is one multiply-high Barrett step (magic = floor(2^32 / m): the quotient
+// estimate is q or q - 1) plus one correction.
+__device__ __forceinline__ void oz_store_residues(uint32_t taddr, uint8_t* dst, int row, int n0, int n, int m) {
+  const uint32_t mu = (uint32_t)m;
+  const uint32_t off = mu << 23;
+  const uint32_t magic = (uint32_t)(0x100000000ULL / mu);
+#pragma unroll 1
+  for (int cc = 0; cc < OZ_BN / 32; ++cc) {
+    uint32_t v[32];
+    tmem_ld32(taddr + 32 * cc, v);
+    tmem_ld_wait();
+    const int col0 = n0 + 32 * cc;
+    if (row < n && col0 < n) {
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          uint32_t r;
+          if (m == 256) {
+            r = v[4 * i + b] & 255u;
+          } else {
+            const uint32_t u = v[4 * i + b] + off;
+            r = u - mu * __umulhi(u, magic);
+            if (r >= mu) r -= mu;
+          }
+          word |= r << (8 * b);
+        }
+        w[i] = word;
+      }
+      *reinterpret_cast<uint4*>(dst + col0) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(dst + col0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const OzGemmArgs g) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_ST * OZ_STAGE);
+  uint64_t* empty = full + OZ_ST;
+  uint64_t* tfull = empty + OZ_ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = g.n;
+  const int tiles_m = (n + OZ_BM - 1) / OZ_BM, tiles_n = (n + OZ_BN - 1) / OZ_BN;
+  const int total = tiles_m * tiles_n * g.num_z * g.nmod;
+  const int KB = (n + OZ_BK - 1) / OZ_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, OZ_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const bool stopped = (g.flag != nullptr && *(volatile const int*)g.flag != 0);
+
+  if (!stopped && warp == 0 && lane == 0) {
+    // ===================== TMA producer =====================
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int plane, m0, n0;
+      if (!oz_tile(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
+      const int z = plane / g.nmod, mod = plane - z * g.nmod;
+      const int pa = (g.a_step ? z : 0) * g.nmod + mod;
+      const int pb = (g.b_step ? (z ^ g.b_xor) : 0) * g.nmod + mod;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sA = smem + stage * OZ_STAGE;
+        mbar_arrive_expect_tx(&full[stage], OZ_STAGE);
+        tma_load_3d(sA, &tmA, &full[stage], kb * OZ_BK, m0, pa);
+        tma_load_3d(sA + OZ_A_BYTES, &tmB, &full[stage], kb * OZ_BK, n0, pb);
+        if (++stage == OZ_ST) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (!stopped && warp == 1 && lane == 0) {
+    // ===================== MMA issuer (one thread) =====================
+    // kind::i8, D int32 (c_format 2), A/B signed int8 (format 1), both K-major, M = 128, N = 256
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
+                           ((uint32_t)(OZ_BM >> 4) << 24);
+    const uint32_t sbase = smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int plane, m0, n0;
+      if (!oz_tile(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * OZ_BN;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a0 = sbase + stage * OZ_STAGE, b0 = a0 + OZ_A_BYTES;
+#pragma unroll
+        for (int k = 0; k < OZ_BK / 32; ++k)
+          umma_i8(d, umma_desc_k_sw128(a0 + 32 * k), umma_desc_k_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+        umma_commit(&empty[stage]);   // frees the smem stage when these MMAs complete
+        if (++stage == OZ_ST) { stage = 0; phase ^= 1; }
+      }
+      umma_commit(&tfull[acc]);       // accumulator ready for the epilogue
+      ++it;
+    }
+  } else if (!stopped && warp >= 2) {
+    // ===================== epilogue: TMEM -> residues (bytes) -> global =====================
+    const int q = warp & 3;   // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int plane, m0, n0;
+      if (!oz_tile(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      const int mod = plane % g.nmod;
+      const int m = (int)c_oz[g.nmod].m[mod];
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int row = m0 + 32 * q + lane;
+      uint8_t* dst = g.R + (long long)plane * g.rpstride + (long long)row * g.ldr;
+      oz_store_residues(tmem_base + ((uint32_t)(32 * q) << 16) + acc * OZ_BN, dst, row, n0, n, m);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, OZ_TMEM_COLS);
+  }
+}
+
+
+// CTA-pair version (cta_group::2): a cluster of 2 CTAs on one TPC computes a 256 x 256 tile with
+// M = 256 MMAs issued by the leader; each CTA stages its own 128 rows of A and 128 rows (N half) of
+// B per k-block, so L2 -> SM traffic per MAC is 2/3 of the single-CTA 128 x 256 tile.  TMA
+// completions of both CTAs count on the leader's full barrier; MMA commits multicast to both CTAs'
+// empty / tmem-full barriers; both CTAs' epilogue warps arrive on the leader's tmem-empty barrier.
+constexpr int OZ2_ST = 6;
+constexpr int OZ2_A_BYTES = 128 * OZ_BK, OZ2_B_BYTES = 128 * OZ_BK, OZ2_STAGE = OZ2_A_BYTES + OZ2_B_BYTES;
+constexpr int OZ2_SMEM = OZ2_ST * OZ2_STAGE + 1024 + 256;
+
+__device__ __forceinline__ bool oz_tile2(const OzGemmArgs& g, int t, int tiles_m, int tiles_n, int& plane, int& m0,
+                                         int& n0) {
+  const int per = tiles_m * tiles_n;
+  plane = t / per;
+  const int r = t - plane * per;
+  const int tm = r / tiles_n;
+  m0 = tm * 256;
+  n0 = (r - tm * tiles_n) * 256;
+  return !(g.sym && m0 > n0 + 255);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
+    oz_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const OzGemmArgs g) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ2_ST * OZ2_STAGE);
+  uint64_t* empty = full + OZ2_ST;
+  uint64_t* tfull = empty + OZ2_ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int n = g.n;
+  const int tiles_m = (n + 255) / 256, tiles_n = (n + 255) / 256;
+  const int total = tiles_m * tiles_n * g.num_z * g.nmod;
+  const int KB = (n + OZ_BK - 1) / OZ_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ2_ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);   // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, OZ_TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const bool stopped = (g.flag != nullptr && *(volatile const int*)g.flag != 0);   // same for both CTAs
+
+  if (!stopped && warp == 0 && lane == 0) {
+    // ===================== TMA producer (both CTAs: own A rows, own B-half rows) =====================
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = pair; t < total; t += npairs) {
+      int plane, m0, n0;
+      if (!oz_tile2(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
+      const int z = plane / g.nmod, mod = plane - z * g.nmod;
+      const int pa = (g.a_step ? z : 0) * g.nmod + mod;
+      const int pb = (g.b_step ? (z ^ g.b_xor) : 0) * g.nmod + mod;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sA = smem + stage * OZ2_STAGE;
+        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * OZ2_STAGE);
+        tma_load_3d_pair(sA, &tmA, &full[stage], kb * OZ_BK, m0 + 128 * (int)rank, pa);
+        tma_load_3d_pair(sA + OZ2_A_BYTES, &tmB, &full[stage], kb * OZ_BK, n0 + 128 * (int)rank, pb);
+        if (++stage == OZ2_ST) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (!stopped && warp == 1 && lane == 0 && rank == 0) {
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                           ((uint32_t)(256 >> 4) << 24);
+    const uint32_t sbase = smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = pair; t < total; t += npairs) {
+      int plane, m0, n0;
+      if (!oz_tile2(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait_cluster(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * OZ_BN;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a0 = sbase + stage * OZ2_STAGE, b0 = a0 + OZ2_A_BYTES;
+#pragma unroll
+        for (int k = 0; k < OZ_BK / 32; ++k)
+          umma_i8_pair(d, umma_desc_k_sw128(a0 + 32 * k), umma_desc_k_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+        umma_commit_pair(&empty[stage], 3);
+        if (++stage == OZ2_ST) { stage = 0; phase ^= 1; }
+      }
+      umma_commit_pair(&tfull[acc], 3);
+      ++it;
+    }
+  } else if (!stopped && warp >= 2) {
+    // ===================== epilogue (both CTAs: their own 128 rows) =====================
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = pair; t < total; t += npairs) {
+      int plane, m0, n0;
+      if (!oz_tile2(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      const int mod = plane % g.nmod;
+      const int m = (int)c_oz[g.nmod].m[mod];
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int row = m0 + 128 * (int)rank + 32 * q + lane;
+      uint8_t* dst = g.R + (long long)plane * g.rpstride + (long long)row * g.ldr;
+      oz_store_residues(tmem_base + ((uint32_t)(32 * q) << 16) + acc * OZ_BN, dst, row, n0, n, m);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, OZ_TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// decode: CRT -> double -> scale -> fused parareal epilogue
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double i128_to_double(i128 v) {   // correctly rounded
+  const bool neg = v < 0;
+  u128 u = neg ? (u128)(-v) : (u128)v;
+  const unsigned long long hi = (unsigned long long)(u >> 64), lo = (unsigned long long)u;
+  double d;
+  if (hi == 0) {
+    d = (double)lo;   // __ull2double_rn
+  } else {
+    const int s = 64 - __clzll((long long)hi);      // bits above the low 64
+    const unsigned long long top = (unsigned long long)(u >> s);
+    const unsigned long long sticky = (lo & ((1ULL << s) - 1ULL)) != 0ULL;
+    d = ldexp((double)(top | sticky), s);
+  }
+  return neg ? -d : d;
+}
+
+__host__ __device__ constexpr uint32_t oz_cmodinv(uint32_t a, uint32_t m) {
+  long long t = 0, nt = 1, r = m, nr = a % m;
+  while (nr) {
+    const long long q = r / nr;
+    const long long t2 = t - q * nt;
+    t = nt;
+    nt = t2;
+    const long long r2 = r - q * nr;
+    r = nr;
+    nr = r2;
+  }
+  return (uint32_t)(t < 0 ? t + m : t);
+}
+
+// CRT of two residues (ra mod MA, rb mod MB) -> residue mod MA*MB (< 2^16), compile-time moduli
+template <uint32_t MA, uint32_t MB>
+__device__ __forceinline__ uint32_t oz_pair(uint32_t ra, uint32_t rb) {
+  constexpr uint32_t inv = oz_cmodinv(MA % MB, MB);
+  const uint32_t d = (rb + 2 * MB - ra) % MB;   // ra < 256 < 2 MB
+  return ra + MA * ((d * inv) % MB);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uint8_t* R, long long rpstride, int ldr,
+                                                   const double* rscale, const double* cscale, int a_step, int b_step,
+                                                   int nmod) {
+  const OzConst& c = c_oz[nmod];
+  if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
+  const int n = p.n;
+  const int cq = (n + 3) >> 2;
+  const long long per_z = (long long)n * cq;
+  const long long items = per_z * p.num_z;
+  const u128 M = ((u128)c.Mhi << 64) | c.Mlo;
+  double part = 0.0;
+  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int z = (int)(it / per_z);
+    const long long r = it - (long long)z * per_z;
+    const int row = (int)(r / cq);
+    const int col = 4 * (int)(r - (long long)row * cq);
+    if (p.sym && row > col + 3) continue;   // strictly lower: written as the mirror of the upper part
+    const uint8_t* src = R + (long long)z * c.nmod * rpstride + (long long)row * ldr + col;
+    uint32_t w4[kOzMaxModuli];
+#pragma unroll
+    for (int t = 0; t < kOzMaxModuli; ++t)
+      w4[t] = (t < nmod) ? *reinterpret_cast<const uint32_t*>(src + t * rpstride) : 0u;   // all loads in flight
+    unsigned long long acc[4][4];
+    double Q[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc[e][0] = acc[e][1] = acc[e][2] = acc[e][3] = 0ULL;
+      Q[e] = 0.0;
+    }
+#define OZ_GROUP(I, MA, MB)                                                                      \
+  if (2 * (I) < nmod) {                                                                        \
+    _Pragma("unroll") for (int e = 0; e < 4; ++e) {                                            \
+      const uint32_t ra = (w4[2 * (I)] >> (8 * e)) & 255u, rb = (w4[2 * (I) + 1] >> (8 * e)) & 255u; \
+      const uint32_t rho = (2 * (I) + 1 < nmod) ? oz_pair<MA, MB>(ra, rb) : ra;                 \
+      _Pragma("unroll") for (int j = 0; j < 4; ++j) acc[e][j] += (unsigned long long)rho * c.pw[I][j]; \
+      Q[e] = fma((double)rho, c.pwf[I], Q[e]);                                                 \
+    }                                                                                          \
+  }
+    OZ_GROUP(0, 256, 255) OZ_GROUP(1, 253, 251) OZ_GROUP(2, 247, 241) OZ_GROUP(3, 239, 233)
+    OZ_GROUP(4, 229, 227) OZ_GROUP(5, 223, 217) OZ_GROUP(6, 211, 199) OZ_GROUP(7, 197, 193)
+#undef OZ_GROUP
+    u128 S[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      S[e] = (u128)acc[e][0] + ((u128)acc[e][1] << 32) + ((u128)acc[e][2] << 64) + ((u128)acc[e][3] << 96);
+    const int za = a_step ? z : 0, zb = b_step ? (z ^ p.b_xor) : 0;
+    const double rs = rscale[(long long)za * n + row];
+    double k4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const unsigned long long qq = (unsigned long long)rint(Q[e]);
+      const i128 v = (i128)(S[e] - M * qq);   // C' in (-M/4, M/4): exact
+      const double cs = (col + e < n) ? cscale[(long long)zb * n + col + e] : 0.0;
+      k4[e] = i128_to_double(v) * rs * cs;
+    }
+    const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
+    epi_apply4<EPI>(p, z, alpha, row, col, n, p.ld, k4, p.sym != 0, true, part);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side: per-stream workspaces, tensor maps, launch sequence
+// ---------------------------------------------------------------------------------------------
+struct OzWork {
+  int8_t* A = nullptr;
+  int8_t* B = nullptr;
+  uint8_t* R = nullptr;
+  double* rs = nullptr;
+  double* cs = nullptr;
+  int* ce = nullptr;
+  size_t capA = 0, capB = 0, capR = 0, capS = 0;
+};
+static std::mutex g_oz_mu;
+static std::map<cudaStream_t, OzWork>& oz_works() {
+  static std::map<cudaStream_t, OzWork> m;
+  return m;
+}
+
+static cudaError_t grow(void** p, size_t* cap, size_t need) {
+  if (*cap >= need) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e == cudaSuccess) *cap = need;
+  return e;
+}
+
+bool g_oz_pair = true;   // CTA-pair (cta_group::2) integer GEMM; false: single-CTA kernel
+
+static int oz_ldk(int n) { return (n + 15) & ~15; }
+static int oz_ldr(int n) { return (n + 31) & ~31; }
+
+cudaError_t oz_reserve(cudaStream_t st, int n, int max_z, int nmod) {
+  std::lock_guard<std::mutex> lk(g_oz_mu);
+  OzWork& w = oz_works()[st];
+  const size_t pk = (size_t)n * oz_ldk(n), pr = (size_t)n * oz_ldr(n);
+  cudaError_t e;
+  if ((e = grow((void**)&w.A, &w.capA, pk * nmod * max_z)) != cudaSuccess) return e;
+  if ((e = grow((void**)&w.B, &w.capB, pk * nmod * max_z)) != cudaSuccess) return e;
+  if ((e = grow((void**)&w.R, &w.capR, pr * nmod * max_z)) != cudaSuccess) return e;
+  const size_t ns = (size_t)n * max_z * sizeof(double);
+  if (w.capS < ns) {
+    size_t c1 = 0, c2 = 0, c3 = 0;
+    if ((e = grow((void**)&w.rs, &c1, ns)) != cudaSuccess) return e;
+    if ((e = grow((void**)&w.cs, &c2, ns)) != cudaSuccess) return e;
+    if (w.ce) cudaFree(w.ce);
+    w.ce = nullptr;
+    if ((e = grow((void**)&w.ce, &c3, (size_t)n * max_z * sizeof(int))) != cudaSuccess) return e;
+    w.capS = ns;
+  }
+  return cudaSuccess;
+}
+
+void oz_release(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_oz_mu);
+  auto it = oz_works().find(st);
+  if (it == oz_works().end()) return;
+  OzWork& w = it->second;
+  cudaFree(w.A);
+  cudaFree(w.B);
+  cudaFree(w.R);
+  cudaFree(w.rs);
+  cudaFree(w.cs);
+  cudaFree(w.ce);
+  oz_works().erase(it);
+}
+
+typedef CUresult (*PFN_encodeTiled_oz)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_oz oz_encoder() {
+  static PFN_encodeTiled_oz fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_oz>(p);
+  });
+  return fn;
+}
+
+// planes: `count` n x n int8 matrices, row stride ldk, K (columns) innermost; box 128 (K) x rows
+static bool oz_map(CUtensorMap* m, const int8_t* base, int n, int ldk, int count, int box_rows) {
+  static std::mutex mu;
+  static std::map<std::tuple<const int8_t*, int, int, int, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(base, n, ldk, count, box_rows);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *m = it->second;
+    return true;
+  }
+  PFN_encodeTiled_oz enc = oz_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)count};
+  cuuint64_t strides[2] = {(cuuint64_t)ldk, (cuuint64_t)n * ldk};
+  cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > 1024) cache.clear();
+  cache[key] = *m;
+  return true;
+}
+
+static int oz_num_sms() {
+  static int s = 0;
+  if (!s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    if (s <= 0) s = 148;
+  }
+  return s;
+}
+
+template <int EPI>
+static cudaError_t launch_decode(const GemmParams& p, const OzWork& w, long long rp, int ldr, int a_step, int b_step,
+                                 const OzConst& c, cudaStream_t st) {
+  const long long items = (long long)p.num_z * p.n * ((p.n + 3) / 4);
+  long long blocks = (items + 255) / 256;
+  const long long cap = (long long)oz_num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_oz_decode<EPI><<<(unsigned)blocks, 256, 0, st>>>(p, w.R, rp, ldr, w.rs, w.cs, a_step, b_step, c.nmod);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st) {
+  if (epi == EPI_RESID) return cudaErrorInvalidValue;
+  const int n = p.n, nz = p.num_z;
+  if (n > 65536) return cudaErrorInvalidValue;   // int32 accumulators: |sum| <= n 128^2 <= 2^30
+  OzConst c;
+  if (!oz_make_const(p.oz_nmod, n, &c)) return cudaErrorInvalidValue;
+  const int nA = A.step ? nz : 1, nB = B.step ? nz : 1;
+  cudaError_t e = oz_init_device();
+  if (e != cudaSuccess) return e;
+  e = oz_reserve(st, n, std::max(nA, nB), c.nmod);
+  if (e != cudaSuccess) return e;
+  OzWork w;
+  {
+    std::lock_guard<std::mutex> lk(g_oz_mu);
+    w = oz_works()[st];
+  }
+  const int ldk = oz_ldk(n), ldr = oz_ldr(n);
+  const long long pk = (long long)n * ldk, pr = (long long)n * ldr;
+  const long long mst = (long long)n * p.ld;
+  // A: rows
+  k_oz_enc_rows<<<dim3(n, nA), kEncThreads, 0, st>>>(A.slab, mst, A.base, A.step, n, p.ld, w.A, pk, ldk, w.rs, c.nmod, c.abits,
+                                                     p.stop_flag);
+  ++g_launches;
+  // B: column exponents, then transposed planes
+  if ((e = cudaMemsetAsync(w.ce, 0x80, (size_t)n * nB * sizeof(int), st)) != cudaSuccess) return e;
+  k_oz_colexp<<<dim3((n + 31) / 32, (n + 255) / 256, nB), 256, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.ce,
+                                                                      p.stop_flag);
+  ++g_launches;
+  k_oz_enc_colsT<<<dim3((n + kTT - 1) / kTT, (n + kTT - 1) / kTT, nB), 256, 0, st>>>(
+      B.slab, mst, B.base, B.step, n, p.ld, w.ce, w.B, pk, ldk, w.cs, c.nmod, c.abits, p.stop_flag);
+  ++g_launches;
+  // integer GEMMs
+  CUtensorMap ma, mb;
+  if (!oz_map(&ma, w.A, n, ldk, nA * c.nmod, OZ_BM)) return cudaErrorInvalidValue;
+  if (!oz_map(&mb, w.B, n, ldk, nB * c.nmod, g_oz_pair ? 128 : OZ_BN)) return cudaErrorInvalidValue;
+  OzGemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.n = n;
+  g.num_z = nz;
+  g.nmod = c.nmod;
+  g.a_step = A.step ? 1 : 0;
+  g.b_step = B.step ? 1 : 0;
+  g.b_xor = B.xr;
+  g.sym = p.sym;
+  g.R = w.R;
+  g.rpstride = pr;
+  g.ldr = ldr;
+  g.flag = p.stop_flag;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ2_SMEM);
+  });
+  if (g_oz_pair) {
+    const long long tiles = (long long)((n + 255) / 256) * ((n + 255) / 256) * nz * c.nmod;
+    const long long grid = 2 * std::min<long long>(tiles, oz_num_sms() / 2);
+    oz_gemm2_kernel<<<(unsigned)grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, g);
+  } else {
+    const long long tiles = (long long)((n + OZ_BM - 1) / OZ_BM) * ((n + OZ_BN - 1) / OZ_BN) * nz * c.nmod;
+    const long long grid = std::min<long long>(tiles, oz_num_sms());
+    oz_gemm_kernel<<<(unsigned)grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, g);
+  }
+  ++g_launches;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // decode + fused epilogue
+  p.b_xor = B.xr;
+  switch (epi) {
+    case EPI_STORE: return launch_decode<EPI_STORE>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
+    case EPI_RK: return launch_decode<EPI_RK>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
+    case EPI_EULER: return launch_decode<EPI_EULER>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
+    case EPI_EULER_CORR: return launch_decode<EPI_EULER_CORR>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
+    case EPI_ACCEL: return launch_decode<EPI_ACCEL>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mfode
