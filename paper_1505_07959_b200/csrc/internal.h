@@ -55,6 +55,7 @@ struct OzConst {
   unsigned long long Mlo, Mhi;         // M = prod m_t (128-bit)
   uint32_t pw[kOzMaxModuli / 2][4];    // CRT weights of the pair groups (m_2i m_2i+1), 32-bit limbs
   double pwf[kOzMaxModuli / 2];        // pair weight / M
+  uint32_t pinv[kOzMaxModuli / 2];     // m_2i^-1 mod m_2i+1 (epilogue pair CRT)
 };
 bool oz_make_const(int nmod, int k, OzConst* c);
 cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);

@@ -94,6 +94,7 @@ bool oz_make_const(int nmod, int k, OzConst* c) {
     const uint32_t inv = modinv_small((uint32_t)(Mi % P), P);
     const u128 w = Mi * inv;
     for (int j = 0; j < 4; ++j) c->pw[i][j] = (uint32_t)(w >> (32 * j));
+    c->pinv[i] = (2 * i + 1 < nmod) ? modinv_small(kOzModuli[2 * i] % kOzModuli[2 * i + 1], kOzModuli[2 * i + 1]) : 0u;
     c->pwf[i] = (double)((long double)w / (long double)M);
   }
   return true;
@@ -266,44 +267,88 @@ __global__ void __launch_bounds__(256) k_oz_enc_colsT(const double* slab, long l
 }
 
 // ---------------------------------------------------------------------------------------------
-// int8 tensor-core GEMM, one modulus per plane: R_t = (A_t B_t^T) mod m_t  (bytes)
+// int8 tensor-core GEMMs: for each modulus m_t, (A_t B_t^T) mod m_t; the residues of the two moduli
+// of a pair (m_2i, m_2i+1) are combined by CRT in the epilogue into one 16-bit residue mod
+// m_2i m_2i+1, so the decode reads and combines half as many residues.
 // ---------------------------------------------------------------------------------------------
-constexpr int OZ_BM = 128, OZ_BN = 256, OZ_BK = 128, OZ_ST = 4;
-constexpr int OZ_A_BYTES = OZ_BM * OZ_BK, OZ_B_BYTES = OZ_BN * OZ_BK, OZ_STAGE = OZ_A_BYTES + OZ_B_BYTES;
-constexpr int OZ_THREADS = 192;   // warp 0: TMA, warp 1: TMEM alloc + MMA issue, warps 2-5: epilogue
-constexpr int OZ_SMEM = OZ_ST * OZ_STAGE + 1024 + 256;
+constexpr int OZ_BK = 128;          // k-bytes per pipeline stage (one 128-byte swizzle row)
+constexpr int OZ_BN = 256;          // N of one MMA / accumulator (int32 TMEM columns)
+constexpr int OZ_THREADS = 192;     // warp 0: TMA, warp 1: TMEM alloc + MMA issue, warps 2-5: epilogue
 constexpr uint32_t OZ_TMEM_COLS = 2 * OZ_BN;   // double-buffered int32 accumulators
+
+// PAIR = 0: one CTA, 128 x 256 tiles, 4 stages of A 128 x 128 + B 256 x 128 bytes.
+// PAIR = 1: CTA pair (cta_group::2), 256 x 256 tiles; each CTA stages its own 128 A rows and its
+//           128-row half of B (6 stages of 32 KB): 2/3 of the L2 -> SM bytes per MAC.
+template <int PAIR>
+struct OzCfg {
+  static constexpr int kTileM = PAIR ? 256 : 128;
+  static constexpr int kBRows = PAIR ? 128 : 256;       // B rows staged per CTA
+  static constexpr int kStages = PAIR ? 6 : 4;
+  static constexpr int kABytes = 128 * OZ_BK, kBBytes = kBRows * OZ_BK, kStage = kABytes + kBBytes;
+  static constexpr int kStash = 128 * 64 * 4;            // first-modulus residues of a pair (32 KB)
+  static constexpr int kSmem = kStages * kStage + kStash + 1024 + 256;
+};
 
 struct OzGemmArgs {
   int n, num_z, nmod;
   int a_step, b_step, b_xor;
   int sym;               // only tiles meeting the upper triangle (row <= col) are computed
-  uint8_t* R;
-  long long rpstride;
+  uint16_t* R;           // pair residues [z * npairs + i][row][ldr]
+  long long rpstride;    // elements per pair plane (n * ldr)
   int ldr;
   const int* flag;
 };
 
-__device__ __forceinline__ bool oz_tile(const OzGemmArgs& g, int t, int tiles_m, int tiles_n, int& plane, int& m0,
-                                        int& n0) {
-  const int per = tiles_m * tiles_n;
-  plane = t / per;
-  const int r = t - plane * per;
+// Work unit u -> (batch z, modulus pair i, tile origin); cnt = moduli in the pair (2, or 1 for the
+// last pair of an odd count).  Units below the diagonal are skipped in symmetric mode.
+struct OzUnit {
+  int z, pi, cnt, m0, n0;
+};
+template <int PAIR>
+__device__ __forceinline__ bool oz_unit(const OzGemmArgs& g, int u, int tiles_m, int tiles_n, OzUnit& o) {
+  const int per = tiles_m * tiles_n, np = (g.nmod + 1) >> 1;
+  const int zp = u / per;
+  const int r = u - zp * per;
   const int tm = r / tiles_n;
-  m0 = tm * OZ_BM;
-  n0 = (r - tm * tiles_n) * OZ_BN;
-  return !(g.sym && m0 > n0 + OZ_BN - 1);   // entirely below the diagonal: skipped in symmetric mode
+  o.z = zp / np;
+  o.pi = zp - o.z * np;
+  o.cnt = min(2, g.nmod - 2 * o.pi);
+  o.m0 = tm * OzCfg<PAIR>::kTileM;
+  o.n0 = (r - tm * tiles_n) * OZ_BN;
+  return !(g.sym && o.m0 > o.n0 + OZ_BN - 1);
 }
 
-// Epilogue of one accumulator tile row slice: 256 int32 columns of TMEM (this warp's lane quadrant,
-// starting at column address taddr) -> residues mod m (bytes) at dst[n0 ..), row `row`.
-// |x| <= k 128^2 <= 2^30 (k <= 2^16), so u = x + m 2^23 is a non-negative 32-bit integer congruent
-// to x, and u mod m is one multiply-high Barrett step (magic = floor(2^32 / m): the quotient
-// estimate is q or q - 1) plus one correction.
-__device__ __forceinline__ void oz_store_residues(uint32_t taddr, uint8_t* dst, int row, int n0, int n, int m) {
-  const uint32_t mu = (uint32_t)m;
-  const uint32_t off = mu << 23;
-  const uint32_t magic = (uint32_t)(0x100000000ULL / mu);
+__device__ __forceinline__ uint32_t oz_barrett(uint32_t u, uint32_t m, uint32_t magic) {   // u mod m, magic = floor(2^32/m)
+  const uint32_t r = u - m * __umulhi(u, magic);
+  return r >= m ? r - m : r;
+}
+// int32 accumulator x (|x| <= k 128^2 <= 2^30 for k <= 2^16) mod m in [0, m): x + m 2^23 is a
+// non-negative 32-bit integer congruent to x.
+__device__ __forceinline__ uint32_t oz_acc_res(uint32_t v, uint32_t m, uint32_t magic) {
+  return (m == 256u) ? (v & 255u) : oz_barrett(v + (m << 23), m, magic);
+}
+
+// First modulus of a pair: residues of this thread's row (256 columns) stashed in shared memory as
+// packed bytes, word i of epilogue thread t at stash[i * 128 + t] (conflict-free).
+__device__ __forceinline__ void oz_epi_stash(uint32_t taddr, uint32_t* stash, uint32_t m) {
+  const uint32_t magic = (uint32_t)(0x100000000ULL / m);
+#pragma unroll 1
+  for (int cc = 0; cc < OZ_BN / 32; ++cc) {
+    uint32_t v[32];
+    tmem_ld32(taddr + 32 * cc, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      stash[(cc * 8 + i) * 128] = oz_acc_res(v[4 * i], m, magic) | (oz_acc_res(v[4 * i + 1], m, magic) << 8) |
+                          (oz_acc_res(v[4 * i + 2], m, magic) << 16) | (oz_acc_res(v[4 * i + 3], m, magic) << 24);
+  }
+}
+
+// Second modulus mb: rho = CRT(r_a mod ma, r_b mod mb) in [0, ma mb) (or r_b alone if !have_a),
+// stored as 16-bit residues at dst[n0 ..) of row `row`.
+__device__ __forceinline__ void oz_epi_combine(uint32_t taddr, const uint32_t* stash, bool have_a, uint32_t ma,
+                                               uint32_t mb, uint32_t inv_a_b, uint16_t* dst, int row, int n0, int n) {
+  const uint32_t magic = (uint32_t)(0x100000000ULL / mb);
 #pragma unroll 1
   for (int cc = 0; cc < OZ_BN / 32; ++cc) {
     uint32_t v[32];
@@ -311,206 +356,80 @@ __device__ __forceinline__ void oz_store_residues(uint32_t taddr, uint8_t* dst, 
     tmem_ld_wait();
     const int col0 = n0 + 32 * cc;
     if (row < n && col0 < n) {
-      uint32_t w[8];
+      uint32_t sa[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 8; ++i) sa[i] = have_a ? stash[(cc * 8 + i) * 128] : 0u;
+      uint32_t w[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
         uint32_t word = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          uint32_t r;
-          if (m == 256) {
-            r = v[4 * i + b] & 255u;
-          } else {
-            const uint32_t u = v[4 * i + b] + off;
-            r = u - mu * __umulhi(u, magic);
-            if (r >= mu) r -= mu;
+        for (int h = 0; h < 2; ++h) {
+          const int e = 2 * i + h;
+          const uint32_t rb = oz_acc_res(v[e], mb, magic);
+          uint32_t rho = rb;
+          if (have_a) {
+            const uint32_t ra = (sa[e >> 2] >> (8 * (e & 3))) & 255u;
+            rho = ra + ma * oz_barrett((rb + 2u * mb - ra) * inv_a_b, mb, magic);
           }
-          word |= r << (8 * b);
+          word |= rho << (16 * h);
         }
         w[i] = word;
       }
-      *reinterpret_cast<uint4*>(dst + col0) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4*>(dst + col0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + col0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d4[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
     }
   }
 }
 
+template <int PAIR>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const OzGemmArgs g) {
+  using Cfg = OzCfg<PAIR>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_ST * OZ_STAGE);
-  uint64_t* empty = full + OZ_ST;
-  uint64_t* tfull = empty + OZ_ST;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* stash_all = reinterpret_cast<uint32_t*>(smem + Cfg::kStages * Cfg::kStage + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int n = g.n;
-  const int tiles_m = (n + OZ_BM - 1) / OZ_BM, tiles_n = (n + OZ_BN - 1) / OZ_BN;
-  const int total = tiles_m * tiles_n * g.num_z * g.nmod;
+  const int tiles_m = (n + Cfg::kTileM - 1) / Cfg::kTileM, tiles_n = (n + OZ_BN - 1) / OZ_BN;
+  const int total = tiles_m * tiles_n * g.num_z * ((g.nmod + 1) >> 1);
   const int KB = (n + OZ_BK - 1) / OZ_BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < OZ_ST; ++s) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], PAIR ? 8 : 4);   // epilogue warps (of both CTAs; the leader's copy is used)
     }
     fence_barrier_init();
     fence_proxy_async();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, OZ_TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  const bool stopped = (g.flag != nullptr && *(volatile const int*)g.flag != 0);
-
-  if (!stopped && warp == 0 && lane == 0) {
-    // ===================== TMA producer =====================
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int plane, m0, n0;
-      if (!oz_tile(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
-      const int z = plane / g.nmod, mod = plane - z * g.nmod;
-      const int pa = (g.a_step ? z : 0) * g.nmod + mod;
-      const int pb = (g.b_step ? (z ^ g.b_xor) : 0) * g.nmod + mod;
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        unsigned char* sA = smem + stage * OZ_STAGE;
-        mbar_arrive_expect_tx(&full[stage], OZ_STAGE);
-        tma_load_3d(sA, &tmA, &full[stage], kb * OZ_BK, m0, pa);
-        tma_load_3d(sA + OZ_A_BYTES, &tmB, &full[stage], kb * OZ_BK, n0, pb);
-        if (++stage == OZ_ST) { stage = 0; phase ^= 1; }
-      }
-    }
-  } else if (!stopped && warp == 1 && lane == 0) {
-    // ===================== MMA issuer (one thread) =====================
-    // kind::i8, D int32 (c_format 2), A/B signed int8 (format 1), both K-major, M = 128, N = 256
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
-                           ((uint32_t)(OZ_BM >> 4) << 24);
-    const uint32_t sbase = smem_u32(smem);
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int plane, m0, n0;
-      if (!oz_tile(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(&tempty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem_base + acc * OZ_BN;
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint32_t a0 = sbase + stage * OZ_STAGE, b0 = a0 + OZ_A_BYTES;
-#pragma unroll
-        for (int k = 0; k < OZ_BK / 32; ++k)
-          umma_i8(d, umma_desc_k_sw128(a0 + 32 * k), umma_desc_k_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
-        umma_commit(&empty[stage]);   // frees the smem stage when these MMAs complete
-        if (++stage == OZ_ST) { stage = 0; phase ^= 1; }
-      }
-      umma_commit(&tfull[acc]);       // accumulator ready for the epilogue
-      ++it;
-    }
-  } else if (!stopped && warp >= 2) {
-    // ===================== epilogue: TMEM -> residues (bytes) -> global =====================
-    const int q = warp & 3;   // TMEM lane quadrant this warp may access
-    int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int plane, m0, n0;
-      if (!oz_tile(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      const int mod = plane % g.nmod;
-      const int m = (int)c_oz[g.nmod].m[mod];
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      const int row = m0 + 32 * q + lane;
-      uint8_t* dst = g.R + (long long)plane * g.rpstride + (long long)row * g.ldr;
-      oz_store_residues(tmem_base + ((uint32_t)(32 * q) << 16) + acc * OZ_BN, dst, row, n0, n, m);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      ++it;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
   if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, OZ_TMEM_COLS);
+    if (PAIR)
+      tmem_alloc2(tmem_slot, OZ_TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, OZ_TMEM_COLS);
   }
-}
-
-
-// CTA-pair version (cta_group::2): a cluster of 2 CTAs on one TPC computes a 256 x 256 tile with
-// M = 256 MMAs issued by the leader; each CTA stages its own 128 rows of A and 128 rows (N half) of
-// B per k-block, so L2 -> SM traffic per MAC is 2/3 of the single-CTA 128 x 256 tile.  TMA
-// completions of both CTAs count on the leader's full barrier; MMA commits multicast to both CTAs'
-// empty / tmem-full barriers; both CTAs' epilogue warps arrive on the leader's tmem-empty barrier.
-constexpr int OZ2_ST = 6;
-constexpr int OZ2_A_BYTES = 128 * OZ_BK, OZ2_B_BYTES = 128 * OZ_BK, OZ2_STAGE = OZ2_A_BYTES + OZ2_B_BYTES;
-constexpr int OZ2_SMEM = OZ2_ST * OZ2_STAGE + 1024 + 256;
-
-__device__ __forceinline__ bool oz_tile2(const OzGemmArgs& g, int t, int tiles_m, int tiles_n, int& plane, int& m0,
-                                         int& n0) {
-  const int per = tiles_m * tiles_n;
-  plane = t / per;
-  const int r = t - plane * per;
-  const int tm = r / tiles_n;
-  m0 = tm * 256;
-  n0 = (r - tm * tiles_n) * 256;
-  return !(g.sym && m0 > n0 + 255);
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
-    oz_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const OzGemmArgs g) {
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ2_ST * OZ2_STAGE);
-  uint64_t* empty = full + OZ2_ST;
-  uint64_t* tfull = empty + OZ2_ST;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int n = g.n;
-  const int tiles_m = (n + 255) / 256, tiles_n = (n + 255) / 256;
-  const int total = tiles_m * tiles_n * g.num_z * g.nmod;
-  const int KB = (n + OZ_BK - 1) / OZ_BK;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < OZ2_ST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8);   // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
-    }
-    fence_barrier_init();
-    fence_proxy_async();
-  }
-  if (warp == 1) tmem_alloc2(tmem_slot, OZ_TMEM_COLS);
   tc_fence_before();
-  cluster_sync_all();
+  if (PAIR)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -518,82 +437,126 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
   const bool stopped = (g.flag != nullptr && *(volatile const int*)g.flag != 0);   // same for both CTAs
 
   if (!stopped && warp == 0 && lane == 0) {
-    // ===================== TMA producer (both CTAs: own A rows, own B-half rows) =====================
+    // ===================== TMA producer =====================
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = pair; t < total; t += npairs) {
-      int plane, m0, n0;
-      if (!oz_tile2(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
-      const int z = plane / g.nmod, mod = plane - z * g.nmod;
-      const int pa = (g.a_step ? z : 0) * g.nmod + mod;
-      const int pb = (g.b_step ? (z ^ g.b_xor) : 0) * g.nmod + mod;
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        unsigned char* sA = smem + stage * OZ2_STAGE;
-        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * OZ2_STAGE);
-        tma_load_3d_pair(sA, &tmA, &full[stage], kb * OZ_BK, m0 + 128 * (int)rank, pa);
-        tma_load_3d_pair(sA + OZ2_A_BYTES, &tmB, &full[stage], kb * OZ_BK, n0 + 128 * (int)rank, pb);
-        if (++stage == OZ2_ST) { stage = 0; phase ^= 1; }
+    for (int u = unit0; u < total; u += nunits_step) {
+      OzUnit o;
+      if (!oz_unit<PAIR>(g, u, tiles_m, tiles_n, o)) continue;
+      for (int sub = 0; sub < o.cnt; ++sub) {
+        const int mod = 2 * o.pi + sub;
+        const int pa = (g.a_step ? o.z : 0) * g.nmod + mod;
+        const int pb = (g.b_step ? (o.z ^ g.b_xor) : 0) * g.nmod + mod;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char* sA = smem + stage * Cfg::kStage;
+          if (PAIR) {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::kStage);
+            tma_load_3d_pair(sA, &tmA, &full[stage], kb * OZ_BK, o.m0 + 128 * (int)rank, pa);
+            tma_load_3d_pair(sA + Cfg::kABytes, &tmB, &full[stage], kb * OZ_BK, o.n0 + 128 * (int)rank, pb);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
+            tma_load_3d(sA, &tmA, &full[stage], kb * OZ_BK, o.m0, pa);
+            tma_load_3d(sA + Cfg::kABytes, &tmB, &full[stage], kb * OZ_BK, o.n0, pb);
+          }
+          if (++stage == Cfg::kStages) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (!stopped && warp == 1 && lane == 0 && rank == 0) {
-    // ===================== MMA issuer (leader CTA, one thread) =====================
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
-                           ((uint32_t)(256 >> 4) << 24);
+    // ===================== MMA issuer (one thread; the leader CTA in pair mode) =====================
+    // kind::i8, D int32 (c_format 2), A/B signed int8 (format 1), both K-major, M = 128/256, N = 256
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
+                           ((uint32_t)(Cfg::kTileM >> 4) << 24);
     const uint32_t sbase = smem_u32(smem);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int t = pair; t < total; t += npairs) {
-      int plane, m0, n0;
-      if (!oz_tile2(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      mbar_wait_cluster(&tempty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem_base + acc * OZ_BN;
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(&full[stage], phase);
+    for (int u = unit0; u < total; u += nunits_step) {
+      OzUnit o;
+      if (!oz_unit<PAIR>(g, u, tiles_m, tiles_n, o)) continue;
+      for (int sub = 0; sub < o.cnt; ++sub, ++it) {
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        if (PAIR)
+          mbar_wait_cluster(&tempty[acc], aph ^ 1);
+        else
+          mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t a0 = sbase + stage * OZ2_STAGE, b0 = a0 + OZ2_A_BYTES;
+        const uint32_t d = tmem_base + acc * OZ_BN;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = sbase + stage * Cfg::kStage, b0 = a0 + Cfg::kABytes;
 #pragma unroll
-        for (int k = 0; k < OZ_BK / 32; ++k)
-          umma_i8_pair(d, umma_desc_k_sw128(a0 + 32 * k), umma_desc_k_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
-        umma_commit_pair(&empty[stage], 3);
-        if (++stage == OZ2_ST) { stage = 0; phase ^= 1; }
+          for (int k = 0; k < OZ_BK / 32; ++k) {
+            const uint64_t ad = umma_desc_k_sw128(a0 + 32 * k), bd = umma_desc_k_sw128(b0 + 32 * k);
+            if (PAIR)
+              umma_i8_pair(d, ad, bd, idesc, (kb | k) != 0);
+            else
+              umma_i8(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          if (PAIR)
+            umma_commit_pair(&empty[stage], 3);   // frees the stage in both CTAs when these MMAs complete
+          else
+            umma_commit(&empty[stage]);
+          if (++stage == Cfg::kStages) { stage = 0; phase ^= 1; }
+        }
+        if (PAIR)
+          umma_commit_pair(&tfull[acc], 3);       // accumulator ready for both CTAs' epilogues
+        else
+          umma_commit(&tfull[acc]);
       }
-      umma_commit_pair(&tfull[acc], 3);
-      ++it;
     }
   } else if (!stopped && warp >= 2) {
-    // ===================== epilogue (both CTAs: their own 128 rows) =====================
-    const int q = warp & 3;
+    // ===================== epilogue: TMEM -> residues -> pair CRT -> 16-bit residues =====================
+    const int q = warp & 3;   // TMEM lane quadrant this warp may access
+    const OzConst& cst = c_oz[g.nmod];
+    const int np = (g.nmod + 1) >> 1;
+    uint32_t* stash = stash_all + (threadIdx.x - 64);
     int it = 0;
-    for (int t = pair; t < total; t += npairs) {
-      int plane, m0, n0;
-      if (!oz_tile2(g, t, tiles_m, tiles_n, plane, m0, n0)) continue;
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      const int mod = plane % g.nmod;
-      const int m = (int)c_oz[g.nmod].m[mod];
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      const int row = m0 + 128 * (int)rank + 32 * q + lane;
-      uint8_t* dst = g.R + (long long)plane * g.rpstride + (long long)row * g.ldr;
-      oz_store_residues(tmem_base + ((uint32_t)(32 * q) << 16) + acc * OZ_BN, dst, row, n0, n, m);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
-      ++it;
+    for (int u = unit0; u < total; u += nunits_step) {
+      OzUnit o;
+      if (!oz_unit<PAIR>(g, u, tiles_m, tiles_n, o)) continue;
+      const int row = o.m0 + 128 * (int)rank + 32 * q + lane;
+      uint16_t* dst = g.R + (long long)(o.z * np + o.pi) * g.rpstride + (long long)row * g.ldr;
+      const uint32_t ma = cst.m[2 * o.pi];
+      for (int sub = 0; sub < o.cnt; ++sub, ++it) {
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + acc * OZ_BN;
+        if (sub == 0 && o.cnt == 2)
+          oz_epi_stash(taddr, stash, ma);
+        else if (sub == 1)
+          oz_epi_combine(taddr, stash, true, ma, cst.m[2 * o.pi + 1], cst.pinv[o.pi], dst, row, o.n0, n);
+        else
+          oz_epi_combine(taddr, stash, false, 1u, ma, 0u, dst, row, o.n0, n);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(&tempty[acc], 0);
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+      }
     }
   }
   tc_fence_before();
-  cluster_sync_all();
+  if (PAIR)
+    cluster_sync_all();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc2(tmem_base, OZ_TMEM_COLS);
+    if (PAIR)
+      tmem_dealloc2(tmem_base, OZ_TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, OZ_TMEM_COLS);
   }
 }
 
@@ -616,30 +579,8 @@ __device__ __forceinline__ double i128_to_double(i128 v) {   // correctly rounde
   return neg ? -d : d;
 }
 
-__host__ __device__ constexpr uint32_t oz_cmodinv(uint32_t a, uint32_t m) {
-  long long t = 0, nt = 1, r = m, nr = a % m;
-  while (nr) {
-    const long long q = r / nr;
-    const long long t2 = t - q * nt;
-    t = nt;
-    nt = t2;
-    const long long r2 = r - q * nr;
-    r = nr;
-    nr = r2;
-  }
-  return (uint32_t)(t < 0 ? t + m : t);
-}
-
-// CRT of two residues (ra mod MA, rb mod MB) -> residue mod MA*MB (< 2^16), compile-time moduli
-template <uint32_t MA, uint32_t MB>
-__device__ __forceinline__ uint32_t oz_pair(uint32_t ra, uint32_t rb) {
-  constexpr uint32_t inv = oz_cmodinv(MA % MB, MB);
-  const uint32_t d = (rb + 2 * MB - ra) % MB;   // ra < 256 < 2 MB
-  return ra + MA * ((d * inv) % MB);
-}
-
 template <int EPI>
-__global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uint8_t* R, long long rpstride, int ldr,
+__global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uint16_t* R, long long rpstride, int ldr,
                                                    const double* rscale, const double* cscale, int a_step, int b_step,
                                                    int nmod) {
   const OzConst& c = c_oz[nmod];
@@ -657,11 +598,12 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
     const int row = (int)(r / cq);
     const int col = 4 * (int)(r - (long long)row * cq);
     if (p.sym && row > col + 3) continue;   // strictly lower: written as the mirror of the upper part
-    const uint8_t* src = R + (long long)z * c.nmod * rpstride + (long long)row * ldr + col;
-    uint32_t w4[kOzMaxModuli];
+    const int np = (nmod + 1) >> 1;
+    const uint16_t* src = R + (long long)z * np * rpstride + (long long)row * ldr + col;
+    uint2 pr4[kOzMaxModuli / 2];
 #pragma unroll
-    for (int t = 0; t < kOzMaxModuli; ++t)
-      w4[t] = (t < nmod) ? *reinterpret_cast<const uint32_t*>(src + t * rpstride) : 0u;   // all loads in flight
+    for (int i = 0; i < kOzMaxModuli / 2; ++i)
+      pr4[i] = (i < np) ? *reinterpret_cast<const uint2*>(src + i * rpstride) : make_uint2(0u, 0u);   // all in flight
     unsigned long long acc[4][4];
     double Q[4];
 #pragma unroll
@@ -669,18 +611,18 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
       acc[e][0] = acc[e][1] = acc[e][2] = acc[e][3] = 0ULL;
       Q[e] = 0.0;
     }
-#define OZ_GROUP(I, MA, MB)                                                                      \
-  if (2 * (I) < nmod) {                                                                        \
-    _Pragma("unroll") for (int e = 0; e < 4; ++e) {                                            \
-      const uint32_t ra = (w4[2 * (I)] >> (8 * e)) & 255u, rb = (w4[2 * (I) + 1] >> (8 * e)) & 255u; \
-      const uint32_t rho = (2 * (I) + 1 < nmod) ? oz_pair<MA, MB>(ra, rb) : ra;                 \
-      _Pragma("unroll") for (int j = 0; j < 4; ++j) acc[e][j] += (unsigned long long)rho * c.pw[I][j]; \
-      Q[e] = fma((double)rho, c.pwf[I], Q[e]);                                                 \
-    }                                                                                          \
-  }
-    OZ_GROUP(0, 256, 255) OZ_GROUP(1, 253, 251) OZ_GROUP(2, 247, 241) OZ_GROUP(3, 239, 233)
-    OZ_GROUP(4, 229, 227) OZ_GROUP(5, 223, 217) OZ_GROUP(6, 211, 199) OZ_GROUP(7, 197, 193)
-#undef OZ_GROUP
+#pragma unroll
+    for (int i = 0; i < kOzMaxModuli / 2; ++i) {
+      if (i < np) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t rho = ((e < 2 ? pr4[i].x : pr4[i].y) >> (16 * (e & 1))) & 0xFFFFu;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[e][j] += (unsigned long long)rho * c.pw[i][j];
+          Q[e] = fma((double)rho, c.pwf[i], Q[e]);
+        }
+      }
+    }
     u128 S[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -706,7 +648,7 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
 struct OzWork {
   int8_t* A = nullptr;
   int8_t* B = nullptr;
-  uint8_t* R = nullptr;
+  uint16_t* R = nullptr;   // pair residues
   double* rs = nullptr;
   double* cs = nullptr;
   int* ce = nullptr;
@@ -740,7 +682,7 @@ cudaError_t oz_reserve(cudaStream_t st, int n, int max_z, int nmod) {
   cudaError_t e;
   if ((e = grow((void**)&w.A, &w.capA, pk * nmod * max_z)) != cudaSuccess) return e;
   if ((e = grow((void**)&w.B, &w.capB, pk * nmod * max_z)) != cudaSuccess) return e;
-  if ((e = grow((void**)&w.R, &w.capR, pr * nmod * max_z)) != cudaSuccess) return e;
+  if ((e = grow((void**)&w.R, &w.capR, pr * 2 * ((nmod + 1) / 2) * max_z)) != cudaSuccess) return e;
   const size_t ns = (size_t)n * max_z * sizeof(double);
   if (w.capS < ns) {
     size_t c1 = 0, c2 = 0, c3 = 0;
@@ -822,16 +764,46 @@ static int oz_num_sms() {
 }
 
 template <int EPI>
-static cudaError_t launch_decode(const GemmParams& p, const OzWork& w, long long rp, int ldr, int a_step, int b_step,
-                                 const OzConst& c, cudaStream_t st) {
+static cudaError_t launch_decode(const GemmParams& p, const uint16_t* R, long long rp, int ldr, const double* rs,
+                                 const double* cs, int a_step, int b_step, int nmod, cudaStream_t st) {
   const long long items = (long long)p.num_z * p.n * ((p.n + 3) / 4);
   long long blocks = (items + 255) / 256;
   const long long cap = (long long)oz_num_sms() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_oz_decode<EPI><<<(unsigned)blocks, 256, 0, st>>>(p, w.R, rp, ldr, w.rs, w.cs, a_step, b_step, c.nmod);
+  k_oz_decode<EPI><<<(unsigned)blocks, 256, 0, st>>>(p, R, rp, ldr, rs, cs, a_step, b_step, nmod);
   ++g_launches;
   return cudaGetLastError();
+}
+
+template <int PAIR>
+static cudaError_t launch_oz_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const OzGemmArgs& g, cudaStream_t st) {
+  using Cfg = OzCfg<PAIR>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(oz_gemm_kernel<PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (PAIR) cudaFuncSetAttribute(oz_gemm_kernel<PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+  });
+  const int n = g.n;
+  const long long units = (long long)((n + Cfg::kTileM - 1) / Cfg::kTileM) * ((n + OZ_BN - 1) / OZ_BN) * g.num_z *
+                          ((g.nmod + 1) / 2);
+  const int slots = PAIR ? oz_num_sms() / 2 : oz_num_sms();
+  const long long grid = (PAIR ? 2 : 1) * std::min<long long>(units, slots);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, oz_gemm_kernel<PAIR>, ma, mb, g);
+  ++g_launches;
+  return e;
 }
 
 cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st) {
@@ -853,22 +825,39 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
   const int ldk = oz_ldk(n), ldr = oz_ldr(n);
   const long long pk = (long long)n * ldk, pr = (long long)n * ldr;
   const long long mst = (long long)n * p.ld;
-  // A: rows
-  k_oz_enc_rows<<<dim3(n, nA), kEncThreads, 0, st>>>(A.slab, mst, A.base, A.step, n, p.ld, w.A, pk, ldk, w.rs, c.nmod, c.abits,
-                                                     p.stop_flag);
+  // A: row-scaled planes
+  k_oz_enc_rows<<<dim3(n, nA), kEncThreads, 0, st>>>(A.slab, mst, A.base, A.step, n, p.ld, w.A, pk, ldk, w.rs, c.nmod,
+                                                     c.abits, p.stop_flag);
   ++g_launches;
-  // B: column exponents, then transposed planes
-  if ((e = cudaMemsetAsync(w.ce, 0x80, (size_t)n * nB * sizeof(int), st)) != cudaSuccess) return e;
-  k_oz_colexp<<<dim3((n + 31) / 32, (n + 255) / 256, nB), 256, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.ce,
-                                                                      p.stop_flag);
-  ++g_launches;
-  k_oz_enc_colsT<<<dim3((n + kTT - 1) / kTT, (n + kTT - 1) / kTT, nB), 256, 0, st>>>(
-      B.slab, mst, B.base, B.step, n, p.ld, w.ce, w.B, pk, ldk, w.cs, c.nmod, c.abits, p.stop_flag);
-  ++g_launches;
-  // integer GEMMs
+  // B: column-scaled planes, transposed to K-major.  In symmetric mode every operand is exactly
+  // symmetric (all iterates are symmetric polynomials in A and the mirrored epilogue keeps them so
+  // bitwise), so column j of B is row j: the row encoder produces the same planes, and an operand
+  // equal to A reuses A's planes outright.
+  const int8_t* planesB = w.B;
+  const double* csB = w.cs;
+  if (p.sym && B.slab == A.slab && B.base == A.base && B.step == A.step && B.xr == 0) {
+    planesB = w.A;
+    csB = w.rs;
+  } else if (p.sym && B.xr == 0) {
+    k_oz_enc_rows<<<dim3(n, nB), kEncThreads, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.B, pk, ldk, w.cs,
+                                                       c.nmod, c.abits, p.stop_flag);
+    ++g_launches;
+  } else {
+    if ((e = cudaMemsetAsync(w.ce, 0x80, (size_t)n * nB * sizeof(int), st)) != cudaSuccess) return e;
+    k_oz_colexp<<<dim3((n + 31) / 32, (n + 255) / 256, nB), 256, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.ce,
+                                                                        p.stop_flag);
+    ++g_launches;
+    k_oz_enc_colsT<<<dim3((n + kTT - 1) / kTT, (n + kTT - 1) / kTT, nB), 256, 0, st>>>(
+        B.slab, mst, B.base, B.step, n, p.ld, w.ce, w.B, pk, ldk, w.cs, c.nmod, c.abits, p.stop_flag);
+    ++g_launches;
+  }
+  // integer GEMMs (pair-combined 16-bit residues)
+  const bool pair = g_oz_pair;
   CUtensorMap ma, mb;
-  if (!oz_map(&ma, w.A, n, ldk, nA * c.nmod, OZ_BM)) return cudaErrorInvalidValue;
-  if (!oz_map(&mb, w.B, n, ldk, nB * c.nmod, g_oz_pair ? 128 : OZ_BN)) return cudaErrorInvalidValue;
+  if (!oz_map(&ma, w.A, n, ldk, nA * c.nmod, 128)) return cudaErrorInvalidValue;
+  if (!oz_map(&mb, planesB, n, ldk, (planesB == w.A ? nA : nB) * c.nmod,
+              pair ? OzCfg<1>::kBRows : OzCfg<0>::kBRows))
+    return cudaErrorInvalidValue;
   OzGemmArgs g;
   memset(&g, 0, sizeof(g));
   g.n = n;
@@ -882,30 +871,16 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
   g.rpstride = pr;
   g.ldr = ldr;
   g.flag = p.stop_flag;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ2_SMEM);
-  });
-  if (g_oz_pair) {
-    const long long tiles = (long long)((n + 255) / 256) * ((n + 255) / 256) * nz * c.nmod;
-    const long long grid = 2 * std::min<long long>(tiles, oz_num_sms() / 2);
-    oz_gemm2_kernel<<<(unsigned)grid, OZ_THREADS, OZ2_SMEM, st>>>(ma, mb, g);
-  } else {
-    const long long tiles = (long long)((n + OZ_BM - 1) / OZ_BM) * ((n + OZ_BN - 1) / OZ_BN) * nz * c.nmod;
-    const long long grid = std::min<long long>(tiles, oz_num_sms());
-    oz_gemm_kernel<<<(unsigned)grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, g);
-  }
-  ++g_launches;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = pair ? launch_oz_gemm<1>(ma, mb, g, st) : launch_oz_gemm<0>(ma, mb, g, st)) != cudaSuccess) return e;
   // decode + fused epilogue
   p.b_xor = B.xr;
   switch (epi) {
-    case EPI_STORE: return launch_decode<EPI_STORE>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
-    case EPI_RK: return launch_decode<EPI_RK>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
-    case EPI_EULER: return launch_decode<EPI_EULER>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
-    case EPI_EULER_CORR: return launch_decode<EPI_EULER_CORR>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
-    case EPI_ACCEL: return launch_decode<EPI_ACCEL>(p, w, pr, ldr, g.a_step, g.b_step, c, st);
+    case EPI_STORE: return launch_decode<EPI_STORE>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_RK: return launch_decode<EPI_RK>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_EULER: return launch_decode<EPI_EULER>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_EULER_CORR:
+      return launch_decode<EPI_EULER_CORR>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_ACCEL: return launch_decode<EPI_ACCEL>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
   }
   return cudaErrorInvalidValue;
 }
