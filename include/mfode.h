@@ -212,7 +212,7 @@ MFODE_API int mfode_dgemm(const double *dA, const double *dB, const double *dC, 
  * modulus) and the Chinese remainder theorem, then scaled back with one correctly rounded
  * conversion.  Error per element <= 2^-(a+1) (2^e_i sum_k |B_kj| + 2^f_j sum_k |A_ik|) + rounding,
  * where 2^e_i > max_k |A_ik|, 2^f_j > max_k |B_kj|.  Deterministic (bitwise reproducible).
- * n_moduli in 2..16.  Same buffers / layout / stream semantics as mfode_dgemm.  Scratch
+ * n_moduli in 2..16, n <= 32768 (int32 accumulation of uint8 residue products).  Same buffers / layout / stream semantics as mfode_dgemm.  Scratch
  * (3 n_moduli n^2 bytes + O(n)) is cached per stream until mfode_release_workspace(stream).
  * Errors: EINVAL, ECUDA, ENOMEM. */
 MFODE_API int mfode_dgemm_emulated(const double *dA, const double *dB, const double *dC, double *dD, int64_t n,

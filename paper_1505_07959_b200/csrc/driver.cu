@@ -1327,7 +1327,7 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     if (value != 0 && (value < 8 || value > kOzMaxModuli))
       return fail(h, MFODE_EINVAL, "emulation needs 0 (off) or 8..%d moduli", kOzMaxModuli);
     OzConst c;
-    if (value != 0 && !oz_make_const((int)value, h->n, &c))
+    if (value != 0 && (h->n > 32768 || !oz_make_const((int)value, h->n, &c)))
       return fail(h, MFODE_EINVAL, "n = %d too large for %lld moduli", h->n, (long long)value);
     if (value && h->small) h->small = false;   // K6 kernels do not go through the GEMM dispatch
     h->oz_nmod = (int)value;
@@ -1427,7 +1427,7 @@ int mfode_dgemm_emulated(const double* dA, const double* dB, const double* dC, d
   if (!dA || !dB || !dD || (beta != 0.0 && !dC)) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (n < 1 || ld < n || (ld * 8) % 16 != 0) return set_global_err(MFODE_EINVAL, "bad n/ld");
   OzConst c;
-  if (n_moduli < 2 || n_moduli > kOzMaxModuli || !oz_make_const(n_moduli, (int)n, &c))
+  if (n > 32768 || n_moduli < 2 || n_moduli > kOzMaxModuli || !oz_make_const(n_moduli, (int)n, &c))
     return set_global_err(MFODE_EINVAL, "n_moduli must be 2..%d and leave >= 8 bits per operand", kOzMaxModuli);
   GemmParams p;
   memset(&p, 0, sizeof(p));

@@ -7,9 +7,10 @@
 //      of the row's max |A_ik|) and rounded to an integer A'_ik, |A'_ik| <= 2^a; every column j of
 //      the right operand B likewise to B'_kj, |B'_kj| <= 2^a.  C' = A' B' is an integer matrix with
 //      |C'_ij| <= k 2^(2a) < M/4, M = m_1 ... m_T (T pairwise-coprime moduli <= 256).
-//   2. for each modulus m_t: the residues (A' mod m_t), (B' mod m_t) fit int8 (symmetric range),
-//      so C'_t = (A' mod m_t)(B' mod m_t) is an exact int32 GEMM on the tensor cores
-//      (|sum| <= k * 128^2 < 2^31 for k < 2^17); its epilogue stores C'_t mod m_t as one byte.
+//   2. for each modulus m_t: the residues (A' mod m_t), (B' mod m_t) in [0, m_t) fit uint8, so
+//      C'_t = (A' mod m_t)(B' mod m_t) is an exact int32 GEMM on the tensor cores (sum <= k 255^2
+//      < 2^31 for k <= 32768); the epilogue reduces it mod m_t and combines the moduli pairwise
+//      (m_2i, m_2i+1) by CRT into one 16-bit residue.
 //   3. decode: C' is recovered EXACTLY from its residues by the Chinese remainder theorem
 //      (C' = sum_t r_t w_t mod M, 128-bit integer arithmetic), converted to double with one
 //      correctly-rounded conversion and scaled back by 2^(e_i + f_j - 2a); the fused parareal
@@ -123,32 +124,30 @@ static cudaError_t oz_init_device() {
 // ---------------------------------------------------------------------------------------------
 // encode
 // ---------------------------------------------------------------------------------------------
-// Residue of the scaled integer x (|x| <= 2^60) modulo the compile-time modulus M, symmetric range:
-// x = x2 2^40 + x1 2^20 + x0 (x0, x1 in [0, 2^20)), x mod M = (x2 c2 + x1 c1 + x0) mod M with
-// c1 = 2^20 mod M, c2 = 2^40 mod M; |x2 c2 + x1 c1 + x0| < 2^29, so 32-bit integer arithmetic with a
-// constant divisor (multiply-high) is exact.
+// Residue in [0, M) of the scaled integer x (|x| <= 2^60) for the compile-time modulus M.  With the
+// bias x' = x + 2^61 >= 0 split as x' = u2 2^40 + u1 2^20 + u0 (u0, u1 < 2^20, u2 < 2^22):
+// x mod M = (u2 c2 + u1 c1 + u0 + (M - b)) mod M, c1 = 2^20 mod M, c2 = 2^40 mod M, b = 2^61 mod M;
+// the sum is < 2^31, so one unsigned 32-bit division by a constant (multiply-high) is exact.
 template <uint32_t M>
-__device__ __forceinline__ int oz_res(int x0, int x1, int x2) {
-  constexpr int c1 = (int)((1ull << 20) % M), c2 = (int)((1ull << 40) % M);
-  const int s = x2 * c2 + x1 * c1 + x0;
-  int r = s % (int)M;
-  if (r < 0) r += (int)M;
-  if (2 * r >= (int)M) r -= (int)M;
-  return r;
+__device__ __forceinline__ uint32_t oz_res(uint32_t u0, uint32_t u1, uint32_t u2) {
+  constexpr uint32_t c1 = (uint32_t)((1ull << 20) % M), c2 = (uint32_t)((1ull << 40) % M);
+  constexpr uint32_t nb = M - (uint32_t)((1ull << 61) % M);
+  return (u2 * c2 + u1 * c1 + u0 + nb) % M;
 }
 
-__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
-  return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) | ((uint32_t)(d & 255) << 24);
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return a | (b << 8) | (c << 16) | (d << 24);
 }
 
-// Writes the residues of 4 consecutive scaled integers to planes t = 0..nmod-1 (plane stride pstride).
-__device__ __forceinline__ void oz_write_residues4(int8_t* dst, long long pstride, const long long (&x)[4], int nmod) {
-  int l0[4], l1[4], l2[4];
+// Writes the residues (uint8, [0, m_t)) of 4 consecutive scaled integers to planes t = 0..nmod-1.
+__device__ __forceinline__ void oz_write_residues4(uint8_t* dst, long long pstride, const long long (&x)[4], int nmod) {
+  uint32_t l0[4], l1[4], l2[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    l0[q] = (int)(x[q] & 0xFFFFF);
-    l1[q] = (int)((x[q] >> 20) & 0xFFFFF);
-    l2[q] = (int)(x[q] >> 40);
+    const unsigned long long xb = (unsigned long long)(x[q] + (1LL << 61));
+    l0[q] = (uint32_t)(xb & 0xFFFFF);
+    l1[q] = (uint32_t)((xb >> 20) & 0xFFFFF);
+    l2[q] = (uint32_t)(xb >> 40);
   }
 #define OZ_PLANE(T, MV)                                                                                 \
   if (T < nmod)                                                                                       \
@@ -171,7 +170,7 @@ constexpr int kEncThreads = 128;
 
 // Left operand: row i of matrix (base + z*step) -> nmod int8 planes [z*nmod + t][i][0..ld_k), K-major.
 __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab, long long mstride, int base, int step,
-                                                              int n, int ld, int8_t* planes, long long pstride,
+                                                              int n, int ld, uint8_t* planes, long long pstride,
                                                               int ldk, double* rscale, int nmod, int abits, const int* flag) {
   if (flag != nullptr && *(volatile const int*)flag != 0) return;
   const int row = blockIdx.x, z = blockIdx.y;
@@ -202,7 +201,7 @@ __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab,
   const int e = (mx > 0.0) ? exp_of_max(mx) : 0;
   const double scale = ldexp(1.0, abits - e);
   if (threadIdx.x == 0) rscale[(long long)z * n + row] = bad_s ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, e - abits);
-  int8_t* dst = planes + (long long)z * nmod * pstride + (long long)row * ldk;
+  uint8_t* dst = planes + (long long)z * nmod * pstride + (long long)row * ldk;
   for (int k = 4 * threadIdx.x; k < ldk; k += 4 * kEncThreads) {
     long long x[4];
 #pragma unroll
@@ -236,7 +235,7 @@ __global__ void k_oz_colexp(const double* slab, long long mstride, int base, int
 // Right operand, pass 2: B'[k][j] -> planes [z*nmod + t][j][k] (transposed: K-major for the MMA).
 constexpr int kTT = 64;   // 64 x 64 transpose tile
 __global__ void __launch_bounds__(256) k_oz_enc_colsT(const double* slab, long long mstride, int base, int step,
-                                                       int n, int ld, const int* colexp, int8_t* planes,
+                                                       int n, int ld, const int* colexp, uint8_t* planes,
                                                        long long pstride, int ldk, double* cscale, int nmod,
                                                        int abits, const int* flag) {
   if (flag != nullptr && *(volatile const int*)flag != 0) return;
@@ -248,7 +247,7 @@ __global__ void __launch_bounds__(256) k_oz_enc_colsT(const double* slab, long l
     tile[kk][jj] = (k0 + kk < n && j0 + jj < n) ? src[(long long)(k0 + kk) * ld + j0 + jj] : 0.0;
   }
   __syncthreads();
-  int8_t* dst = planes + (long long)z * nmod * pstride;
+  uint8_t* dst = planes + (long long)z * nmod * pstride;
   for (int w = threadIdx.x; w < kTT * (kTT / 4); w += 256) {
     const int jj = w / (kTT / 4), kq = w % (kTT / 4);
     const int j = j0 + jj, k = k0 + 4 * kq;
@@ -322,10 +321,10 @@ __device__ __forceinline__ uint32_t oz_barrett(uint32_t u, uint32_t m, uint32_t 
   const uint32_t r = u - m * __umulhi(u, magic);
   return r >= m ? r - m : r;
 }
-// int32 accumulator x (|x| <= k 128^2 <= 2^30 for k <= 2^16) mod m in [0, m): x + m 2^23 is a
-// non-negative 32-bit integer congruent to x.
+// int32 accumulator (a sum of k products of residues in [0, 256): 0 <= v <= k 255^2 < 2^31 for
+// k <= 32768) mod m in [0, m)
 __device__ __forceinline__ uint32_t oz_acc_res(uint32_t v, uint32_t m, uint32_t magic) {
-  return (m == 256u) ? (v & 255u) : oz_barrett(v + (m << 23), m, magic);
+  return (m == 256u) ? (v & 255u) : oz_barrett(v, m, magic);
 }
 
 // First modulus of a pair: residues of this thread's row (256 columns) stashed in shared memory as
@@ -467,8 +466,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     }
   } else if (!stopped && warp == 1 && lane == 0 && rank == 0) {
     // ===================== MMA issuer (one thread; the leader CTA in pair mode) =====================
-    // kind::i8, D int32 (c_format 2), A/B signed int8 (format 1), both K-major, M = 128/256, N = 256
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
+    // kind::i8, D int32 (c_format 2), A/B unsigned 8-bit (format 0), both K-major, M = 128/256, N = 256
+    const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
                            ((uint32_t)(Cfg::kTileM >> 4) << 24);
     const uint32_t sbase = smem_u32(smem);
     int stage = 0;
@@ -646,8 +645,8 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
 // host side: per-stream workspaces, tensor maps, launch sequence
 // ---------------------------------------------------------------------------------------------
 struct OzWork {
-  int8_t* A = nullptr;
-  int8_t* B = nullptr;
+  uint8_t* A = nullptr;
+  uint8_t* B = nullptr;
   uint16_t* R = nullptr;   // pair residues
   double* rs = nullptr;
   double* cs = nullptr;
@@ -727,9 +726,9 @@ static PFN_encodeTiled_oz oz_encoder() {
 }
 
 // planes: `count` n x n int8 matrices, row stride ldk, K (columns) innermost; box 128 (K) x rows
-static bool oz_map(CUtensorMap* m, const int8_t* base, int n, int ldk, int count, int box_rows) {
+static bool oz_map(CUtensorMap* m, const uint8_t* base, int n, int ldk, int count, int box_rows) {
   static std::mutex mu;
-  static std::map<std::tuple<const int8_t*, int, int, int, int>, CUtensorMap> cache;
+  static std::map<std::tuple<const uint8_t*, int, int, int, int>, CUtensorMap> cache;
   std::lock_guard<std::mutex> lk(mu);
   auto key = std::make_tuple(base, n, ldk, count, box_rows);
   auto it = cache.find(key);
@@ -743,7 +742,7 @@ static bool oz_map(CUtensorMap* m, const int8_t* base, int n, int ldk, int count
   cuuint64_t strides[2] = {(cuuint64_t)ldk, (cuuint64_t)n * ldk};
   cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
@@ -809,7 +808,7 @@ static cudaError_t launch_oz_gemm(const CUtensorMap& ma, const CUtensorMap& mb, 
 cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st) {
   if (epi == EPI_RESID) return cudaErrorInvalidValue;
   const int n = p.n, nz = p.num_z;
-  if (n > 65536) return cudaErrorInvalidValue;   // int32 accumulators: |sum| <= n 128^2 <= 2^30
+  if (n > 32768) return cudaErrorInvalidValue;   // int32 accumulators: sum <= n 255^2 < 2^31
   OzConst c;
   if (!oz_make_const(p.oz_nmod, n, &c)) return cudaErrorInvalidValue;
   const int nA = A.step ? nz : 1, nB = B.step ? nz : 1;
@@ -833,7 +832,7 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
   // symmetric (all iterates are symmetric polynomials in A and the mirrored epilogue keeps them so
   // bitwise), so column j of B is row j: the row encoder produces the same planes, and an operand
   // equal to A reuses A's planes outright.
-  const int8_t* planesB = w.B;
+  const uint8_t* planesB = w.B;
   const double* csB = w.cs;
   if (p.sym && B.slab == A.slab && B.base == A.base && B.step == A.step && B.xr == 0) {
     planesB = w.A;
