@@ -299,21 +299,38 @@ struct OzGemmArgs {
 };
 
 // Work unit u -> (batch z, modulus pair i, tile origin); cnt = moduli in the pair (2, or 1 for the
-// last pair of an odd count).  Units below the diagonal are skipped in symmetric mode.
+// last pair of an odd count).  Symmetric mode: the pair kernel's square 256 x 256 tile grid is
+// enumerated over its upper triangle only (no idle units); the single-CTA kernel skips units
+// strictly below the diagonal.
 struct OzUnit {
   int z, pi, cnt, m0, n0;
 };
 template <int PAIR>
+__device__ __forceinline__ int oz_units_per_plane(const OzGemmArgs& g, int tiles_m, int tiles_n) {
+  return (PAIR && g.sym) ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n;
+}
+template <int PAIR>
 __device__ __forceinline__ bool oz_unit(const OzGemmArgs& g, int u, int tiles_m, int tiles_n, OzUnit& o) {
-  const int per = tiles_m * tiles_n, np = (g.nmod + 1) >> 1;
+  const int per = oz_units_per_plane<PAIR>(g, tiles_m, tiles_n), np = (g.nmod + 1) >> 1;
   const int zp = u / per;
-  const int r = u - zp * per;
-  const int tm = r / tiles_n;
+  int r = u - zp * per;
+  int tm, tn;
+  if (PAIR && g.sym) {
+    tm = 0;
+    while (r >= tiles_n - tm) {
+      r -= tiles_n - tm;
+      ++tm;
+    }
+    tn = tm + r;
+  } else {
+    tm = r / tiles_n;
+    tn = r - tm * tiles_n;
+  }
   o.z = zp / np;
   o.pi = zp - o.z * np;
   o.cnt = min(2, g.nmod - 2 * o.pi);
   o.m0 = tm * OzCfg<PAIR>::kTileM;
-  o.n0 = (r - tm * tiles_n) * OZ_BN;
+  o.n0 = tn * OZ_BN;
   return !(g.sym && o.m0 > o.n0 + OZ_BN - 1);
 }
 
@@ -403,7 +420,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const int nunits_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int n = g.n;
   const int tiles_m = (n + Cfg::kTileM - 1) / Cfg::kTileM, tiles_n = (n + OZ_BN - 1) / OZ_BN;
-  const int total = tiles_m * tiles_n * g.num_z * ((g.nmod + 1) >> 1);
+  const int total = oz_units_per_plane<PAIR>(g, tiles_m, tiles_n) * g.num_z * ((g.nmod + 1) >> 1);
   const int KB = (n + OZ_BK - 1) / OZ_BK;
 
   if (threadIdx.x == 0) {
@@ -582,21 +599,20 @@ template <int EPI>
 __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uint16_t* R, long long rpstride, int ldr,
                                                    const double* rscale, const double* cscale, int a_step, int b_step,
                                                    int nmod) {
+  // block = 4 rows x 256 columns (64 threads x 4 columns per row); grid (column blocks, row
+  // blocks, batch).  In symmetric mode blocks strictly below the diagonal exit at once.
   const OzConst& c = c_oz[nmod];
   if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
   const int n = p.n;
-  const int cq = (n + 3) >> 2;
-  const long long per_z = (long long)n * cq;
-  const long long items = per_z * p.num_z;
+  const int col = blockIdx.x * 256 + 4 * (threadIdx.x & 63);
+  const int row = blockIdx.y * 4 + (threadIdx.x >> 6);
+  const int z = blockIdx.z;
+  if (p.sym && blockIdx.y * 4 > blockIdx.x * 256 + 255) return;
   const u128 M = ((u128)c.Mhi << 64) | c.Mlo;
   double part = 0.0;
-  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (long long)gridDim.x * blockDim.x) {
-    const int z = (int)(it / per_z);
-    const long long r = it - (long long)z * per_z;
-    const int row = (int)(r / cq);
-    const int col = 4 * (int)(r - (long long)row * cq);
-    if (p.sym && row > col + 3) continue;   // strictly lower: written as the mirror of the upper part
+  {
+    if (row >= n || col >= n) return;
+    if (p.sym && row > col + 3) return;   // strictly lower: written as the mirror of the upper part
     const int np = (nmod + 1) >> 1;
     const uint16_t* src = R + (long long)z * np * rpstride + (long long)row * ldr + col;
     uint2 pr4[kOzMaxModuli / 2];
@@ -765,12 +781,8 @@ static int oz_num_sms() {
 template <int EPI>
 static cudaError_t launch_decode(const GemmParams& p, const uint16_t* R, long long rp, int ldr, const double* rs,
                                  const double* cs, int a_step, int b_step, int nmod, cudaStream_t st) {
-  const long long items = (long long)p.num_z * p.n * ((p.n + 3) / 4);
-  long long blocks = (items + 255) / 256;
-  const long long cap = (long long)oz_num_sms() * 8;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  k_oz_decode<EPI><<<(unsigned)blocks, 256, 0, st>>>(p, R, rp, ldr, rs, cs, a_step, b_step, nmod);
+  const dim3 grid((p.n + 255) / 256, (p.n + 3) / 4, p.num_z);
+  k_oz_decode<EPI><<<grid, 256, 0, st>>>(p, R, rp, ldr, rs, cs, a_step, b_step, nmod);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -784,8 +796,8 @@ static cudaError_t launch_oz_gemm(const CUtensorMap& ma, const CUtensorMap& mb, 
     if (PAIR) cudaFuncSetAttribute(oz_gemm_kernel<PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   });
   const int n = g.n;
-  const long long units = (long long)((n + Cfg::kTileM - 1) / Cfg::kTileM) * ((n + OZ_BN - 1) / OZ_BN) * g.num_z *
-                          ((g.nmod + 1) / 2);
+  const long long tm = (n + Cfg::kTileM - 1) / Cfg::kTileM, tn = (n + OZ_BN - 1) / OZ_BN;
+  const long long units = ((PAIR && g.sym) ? tn * (tn + 1) / 2 : tm * tn) * g.num_z * ((g.nmod + 1) / 2);
   const int slots = PAIR ? oz_num_sms() / 2 : oz_num_sms();
   const long long grid = (PAIR ? 2 : 1) * std::min<long long>(units, slots);
   cudaLaunchConfig_t cfg = {};
