@@ -133,6 +133,7 @@ struct mfode_ctx {
   bool overlap = true;
   int fine_batch_opt = 0;
   double normA = 0.0;        // ||A||_F
+  unsigned long long mat_gen = 0;   // content generation of A / B (emulated-GEMM encoding cache key)
   std::vector<mfode::Rank> ranks;
   // modified parareal (Algorithm 3): F-orthonormal basis Q of S^k, fine images F(Q), scratch
   double* Qb = nullptr;
@@ -239,7 +240,7 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     GemmParams q = base_params(h, num_z);
     q.Y_out = MatRef{Wbuf, me};
     q.stop_flag = p.stop_flag;
-    Operand Bop{h->B, 1, 0, 0};
+    Operand Bop{h->B, 1, 0, 0, 0, h->mat_gen};
     CUDA_TRY(h, launch_gemm(EPI_STORE, h->tile, Bop, Y, q, st));
     if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
     Operand Wop{Wbuf, Wcount, 0, 1};
@@ -256,7 +257,7 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
     p.alpha = 1.0;
     p.beta = 0.0;
-    Operand Aop{h->A, 1, 0, 0};
+    Operand Aop{h->A, 1, 0, 0, 0, h->mat_gen};
     CUDA_TRY(h, launch_gemm(epi, h->tile, Aop, Y, p, st));
   } else {   // MFODE_FLOW_TRIG: the batch runs over sub-matrices (X, Y) of each state:
              // K_X = A Y (even z), K_Y = -A X (odd z)  -- eq. (eqB) P:448-456 with X0 = 0
@@ -264,7 +265,7 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     p.alpha = 1.0;
     p.beta = 0.0;
     p.alt_sign = 1;
-    Operand Aop{h->A, 1, 0, 0};
+    Operand Aop{h->A, 1, 0, 0, 0, h->mat_gen};
     Operand Ysw = Y;
     Ysw.xr = 1;
     CUDA_TRY(h, launch_gemm(epi, h->tile, Aop, Ysw, p, st));
@@ -532,7 +533,7 @@ static int enqueue_residual(mfode_ctx* h, Rank& R, const double* slab, int count
   double denom;
   if (h->flow == MFODE_FLOW_INVERSE) {
     p.shift = 1.0;
-    Operand Aop{h->A, 1, 0, 0};
+    Operand Aop{h->A, 1, 0, 0, 0, h->mat_gen};
     Operand Xop{slab, count, idx, 0};
     CUDA_TRY(h, launch_gemm(EPI_RESID, tile, Aop, Xop, p, R.coarse));
     denom = sqrt((double)h->n);
@@ -625,6 +626,8 @@ static void free_rank(mfode_ctx* h, Rank& R) {
 
 // A (device, leading dim ld_src) -> h->A (ld), B = I - A, ||A||_F
 static int load_matrix(mfode_ctx* h, const double* src, bool host, size_t ld_src, cudaStream_t st) {
+  static std::atomic<unsigned long long> gen{0};
+  h->mat_gen = ++gen;   // A and B change: cached encodings keyed by the old generation are never hit again
   CUDA_TRY(h, cudaMemcpy2DAsync(h->A, h->ld * sizeof(double), src, ld_src * sizeof(double), h->n * sizeof(double),
                                 h->n, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
   if (h->B) CUDA_TRY(h, launch_i_minus(h->B, h->A, h->n, h->ld, st));
@@ -1381,10 +1384,12 @@ void mfode_destroy(mfode_ctx* h) {
   for (auto& R : h->ranks) free_rank(h, R);
   const size_t me = mat_elems(h);
   if (h->A) {
+    oz_forget(h->A);
     forget_maps(h->A, h->A + me);
     cudaFree(h->A);
   }
   if (h->B) {
+    oz_forget(h->B);
     forget_maps(h->B, h->B + me);
     cudaFree(h->B);
   }
@@ -1564,7 +1569,7 @@ int mfode_accel_inverse(const double* A, const double* X0, const double* E0, int
     p.X_in = MatRef{cur, (long long)me};
     p.S = MatRef{cur + me, 0};          // even z reads u at the same position
     p.X_out = MatRef{nxt, (long long)me};
-    Operand Aop{h->A, 1, 0, 0};
+    Operand Aop{h->A, 1, 0, 0, 0, h->mat_gen};
     Operand Sop{cur, 2, 0, 1};
     CUDA_TRY(h, launch_gemm(EPI_ACCEL, h->tile, Aop, Sop, p, st));
     std::swap(cur, nxt);

@@ -18,6 +18,8 @@ struct Operand {
   int base;
   int step;
   int xr = 0;   // B operand only: batch z reads matrix base + (z ^ xr) * step (trig block pairs)
+  unsigned long long cache_key = 0;   // != 0: a constant matrix (step 0) whose emulated-GEMM encoding may be
+                                      // cached per stream; the key changes whenever its content does
 };
 
 extern std::atomic<long long> g_launches;
@@ -55,12 +57,14 @@ struct OzConst {
   unsigned long long Mlo, Mhi;         // M = prod m_t (128-bit)
   uint32_t pw[kOzMaxModuli / 2][4];    // CRT weights of the pair groups (m_2i m_2i+1), 32-bit limbs
   double pwf[kOzMaxModuli / 2];        // pair weight / M
+  uint32_t pwq[kOzMaxModuli / 2];      // pair weight / M in 0.32 fixed point (decode quotient)
   uint32_t pinv[kOzMaxModuli / 2];     // m_2i^-1 mod m_2i+1 (epilogue pair CRT)
 };
 bool oz_make_const(int nmod, int k, OzConst* c);
 cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
 cudaError_t oz_reserve(cudaStream_t st, int n, int max_z, int nmod);
 void oz_release(cudaStream_t st);
+void oz_forget(const double* ptr);   // drop cached encodings of a matrix about to be freed
 extern bool g_oz_pair;   // option "oz_pair" (process-wide)
 int choose_tile(int n, int num_z, bool sym = false);
 long long gemm_tiles(int tile, int n, int num_z, bool sym = false);

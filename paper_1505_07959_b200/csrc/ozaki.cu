@@ -35,6 +35,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "gemm.cuh"
 #include "internal.h"
@@ -97,6 +98,7 @@ bool oz_make_const(int nmod, int k, OzConst* c) {
     for (int j = 0; j < 4; ++j) c->pw[i][j] = (uint32_t)(w >> (32 * j));
     c->pinv[i] = (2 * i + 1 < nmod) ? modinv_small(kOzModuli[2 * i] % kOzModuli[2 * i + 1], kOzModuli[2 * i + 1]) : 0u;
     c->pwf[i] = (double)((long double)w / (long double)M);
+    c->pwq[i] = (uint32_t)std::floor((long double)w / (long double)M * 4294967296.0L);   // w/M in 0.32 fixed point
   }
   return true;
 }
@@ -619,12 +621,13 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
 #pragma unroll
     for (int i = 0; i < kOzMaxModuli / 2; ++i)
       pr4[i] = (i < np) ? *reinterpret_cast<const uint2*>(src + i * rpstride) : make_uint2(0u, 0u);   // all in flight
-    unsigned long long acc[4][4];
-    double Q[4];
+    // S = sum_i rho_i w_i mod 2^128 in 32-bit limbs (64-bit partial sums, < 2^51), and the CRT
+    // quotient round(sum_i rho_i w_i / M) from 0.32 fixed-point weights (error < 8 * 2^16 * 2^-32).
+    unsigned long long acc[4][4], Q[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       acc[e][0] = acc[e][1] = acc[e][2] = acc[e][3] = 0ULL;
-      Q[e] = 0.0;
+      Q[e] = 0ULL;
     }
 #pragma unroll
     for (int i = 0; i < kOzMaxModuli / 2; ++i) {
@@ -634,7 +637,7 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
           const uint32_t rho = ((e < 2 ? pr4[i].x : pr4[i].y) >> (16 * (e & 1))) & 0xFFFFu;
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[e][j] += (unsigned long long)rho * c.pw[i][j];
-          Q[e] = fma((double)rho, c.pwf[i], Q[e]);
+          Q[e] += (unsigned long long)rho * c.pwq[i];
         }
       }
     }
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
     double k4[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const unsigned long long qq = (unsigned long long)rint(Q[e]);
+      const unsigned long long qq = (Q[e] + 0x80000000ULL) >> 32;
       const i128 v = (i128)(S[e] - M * qq);   // C' in (-M/4, M/4): exact
       const double cs = (col + e < n) ? cscale[(long long)zb * n + col + e] : 0.0;
       k4[e] = i128_to_double(v) * rs * cs;
@@ -660,7 +663,18 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
 // ---------------------------------------------------------------------------------------------
 // host side: per-stream workspaces, tensor maps, launch sequence
 // ---------------------------------------------------------------------------------------------
+// encoding of a constant operand (Operand::cache_key != 0), kept per stream
+struct OzCached {
+  const double* ptr;
+  unsigned long long key;
+  int side;   // 0: row-scaled planes, 1: column-scaled (transposed) planes
+  int nmod, n, ld;
+  uint8_t* planes;
+  double* scale;
+};
+
 struct OzWork {
+  std::vector<OzCached> cached;
   uint8_t* A = nullptr;
   uint8_t* B = nullptr;
   uint16_t* R = nullptr;   // pair residues
@@ -716,6 +730,10 @@ void oz_release(cudaStream_t st) {
   auto it = oz_works().find(st);
   if (it == oz_works().end()) return;
   OzWork& w = it->second;
+  for (auto& c : w.cached) {
+    cudaFree(c.planes);
+    cudaFree(c.scale);
+  }
   cudaFree(w.A);
   cudaFree(w.B);
   cudaFree(w.R);
@@ -723,6 +741,61 @@ void oz_release(cudaStream_t st) {
   cudaFree(w.cs);
   cudaFree(w.ce);
   oz_works().erase(it);
+}
+
+void oz_forget(const double* ptr) {
+  std::lock_guard<std::mutex> lk(g_oz_mu);
+  for (auto& kv : oz_works()) {
+    auto& v = kv.second.cached;
+    for (size_t i = 0; i < v.size();) {
+      if (v[i].ptr == ptr) {
+        cudaStreamSynchronize(kv.first);
+        cudaFree(v[i].planes);
+        cudaFree(v[i].scale);
+        v.erase(v.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+  }
+}
+
+// cached encoding of (ptr, key, side, nmod, n, ld) on stream st: returns true and the buffers if
+// present; otherwise allocates them (fresh = true: the caller encodes into them)
+static cudaError_t oz_cache_get(cudaStream_t st, const double* ptr, unsigned long long key, int side, int nmod, int n,
+                                int ld, uint8_t** planes, double** scale, bool* fresh) {
+  std::lock_guard<std::mutex> lk(g_oz_mu);
+  OzWork& w = oz_works()[st];
+  for (auto& c : w.cached)
+    if (c.ptr == ptr && c.key == key && c.side == side && c.nmod == nmod && c.n == n && c.ld == ld) {
+      *planes = c.planes;
+      *scale = c.scale;
+      *fresh = false;
+      return cudaSuccess;
+    }
+  // stale generations of the same matrix are dropped (the stream orders their last use)
+  for (size_t i = 0; i < w.cached.size();) {
+    if (w.cached[i].ptr == ptr && w.cached[i].key != key) {
+      cudaStreamSynchronize(st);
+      cudaFree(w.cached[i].planes);
+      cudaFree(w.cached[i].scale);
+      w.cached.erase(w.cached.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+  OzCached c{ptr, key, side, nmod, n, ld, nullptr, nullptr};
+  cudaError_t e = cudaMalloc(&c.planes, (size_t)nmod * n * ((n + 15) & ~15));
+  if (e == cudaSuccess) e = cudaMalloc(&c.scale, (size_t)n * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaFree(c.planes);
+    return e;
+  }
+  w.cached.push_back(c);
+  *planes = c.planes;
+  *scale = c.scale;
+  *fresh = true;
+  return cudaSuccess;
 }
 
 typedef CUresult (*PFN_encodeTiled_oz)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -836,37 +909,61 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
   const int ldk = oz_ldk(n), ldr = oz_ldr(n);
   const long long pk = (long long)n * ldk, pr = (long long)n * ldr;
   const long long mst = (long long)n * p.ld;
-  // A: row-scaled planes
-  k_oz_enc_rows<<<dim3(n, nA), kEncThreads, 0, st>>>(A.slab, mst, A.base, A.step, n, p.ld, w.A, pk, ldk, w.rs, c.nmod,
-                                                     c.abits, p.stop_flag);
-  ++g_launches;
+  // A: row-scaled planes (a constant operand's encoding is cached per stream)
+  uint8_t* planesA = w.A;
+  double* rsA = w.rs;
+  bool encA = true;
+  if (A.step == 0 && A.cache_key != 0) {
+    if ((e = oz_cache_get(st, A.slab + (size_t)A.base * mst, A.cache_key, 0, c.nmod, n, p.ld, &planesA, &rsA, &encA)) !=
+        cudaSuccess)
+      return e;
+  }
+  if (encA) {
+    k_oz_enc_rows<<<dim3(n, nA), kEncThreads, 0, st>>>(A.slab, mst, A.base, A.step, n, p.ld, planesA, pk, ldk, rsA,
+                                                       c.nmod, c.abits, A.cache_key ? nullptr : p.stop_flag);
+    ++g_launches;
+  }
   // B: column-scaled planes, transposed to K-major.  In symmetric mode every operand is exactly
   // symmetric (all iterates are symmetric polynomials in A and the mirrored epilogue keeps them so
   // bitwise), so column j of B is row j: the row encoder produces the same planes, and an operand
   // equal to A reuses A's planes outright.
   const uint8_t* planesB = w.B;
   const double* csB = w.cs;
-  if (p.sym && B.slab == A.slab && B.base == A.base && B.step == A.step && B.xr == 0) {
-    planesB = w.A;
-    csB = w.rs;
-  } else if (p.sym && B.xr == 0) {
-    k_oz_enc_rows<<<dim3(n, nB), kEncThreads, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.B, pk, ldk, w.cs,
-                                                       c.nmod, c.abits, p.stop_flag);
-    ++g_launches;
+  const bool same_as_A = (B.slab == A.slab && B.base == A.base && B.step == A.step && B.xr == 0);
+  if (p.sym && same_as_A) {
+    planesB = planesA;
+    csB = rsA;
   } else {
-    if ((e = cudaMemsetAsync(w.ce, 0x80, (size_t)n * nB * sizeof(int), st)) != cudaSuccess) return e;
-    k_oz_colexp<<<dim3((n + 31) / 32, (n + 255) / 256, nB), 256, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.ce,
-                                                                        p.stop_flag);
-    ++g_launches;
-    k_oz_enc_colsT<<<dim3((n + kTT - 1) / kTT, (n + kTT - 1) / kTT, nB), 256, 0, st>>>(
-        B.slab, mst, B.base, B.step, n, p.ld, w.ce, w.B, pk, ldk, w.cs, c.nmod, c.abits, p.stop_flag);
-    ++g_launches;
+    uint8_t* pb = w.B;
+    double* cb = w.cs;
+    bool encB = true;
+    if (B.step == 0 && B.cache_key != 0) {
+      if ((e = oz_cache_get(st, B.slab + (size_t)B.base * mst, B.cache_key, p.sym ? 0 : 1, c.nmod, n, p.ld, &pb, &cb,
+                            &encB)) != cudaSuccess)
+        return e;
+    }
+    const int* flagB = B.cache_key ? nullptr : p.stop_flag;   // a cached encoding must be complete
+    if (encB && p.sym && B.xr == 0) {
+      k_oz_enc_rows<<<dim3(n, nB), kEncThreads, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, pb, pk, ldk, cb, c.nmod,
+                                                         c.abits, flagB);
+      ++g_launches;
+    } else if (encB) {
+      if ((e = cudaMemsetAsync(w.ce, 0x80, (size_t)n * nB * sizeof(int), st)) != cudaSuccess) return e;
+      k_oz_colexp<<<dim3((n + 31) / 32, (n + 255) / 256, nB), 256, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.ce,
+                                                                          flagB);
+      ++g_launches;
+      k_oz_enc_colsT<<<dim3((n + kTT - 1) / kTT, (n + kTT - 1) / kTT, nB), 256, 0, st>>>(
+          B.slab, mst, B.base, B.step, n, p.ld, w.ce, pb, pk, ldk, cb, c.nmod, c.abits, flagB);
+      ++g_launches;
+    }
+    planesB = pb;
+    csB = cb;
   }
   // integer GEMMs (pair-combined 16-bit residues)
   const bool pair = g_oz_pair;
   CUtensorMap ma, mb;
-  if (!oz_map(&ma, w.A, n, ldk, nA * c.nmod, 128)) return cudaErrorInvalidValue;
-  if (!oz_map(&mb, planesB, n, ldk, (planesB == w.A ? nA : nB) * c.nmod,
+  if (!oz_map(&ma, planesA, n, ldk, nA * c.nmod, 128)) return cudaErrorInvalidValue;
+  if (!oz_map(&mb, planesB, n, ldk, (planesB == planesA ? nA : nB) * c.nmod,
               pair ? OzCfg<1>::kBRows : OzCfg<0>::kBRows))
     return cudaErrorInvalidValue;
   OzGemmArgs g;
@@ -886,12 +983,12 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
   // decode + fused epilogue
   p.b_xor = B.xr;
   switch (epi) {
-    case EPI_STORE: return launch_decode<EPI_STORE>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
-    case EPI_RK: return launch_decode<EPI_RK>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
-    case EPI_EULER: return launch_decode<EPI_EULER>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_STORE: return launch_decode<EPI_STORE>(p, w.R, pr, ldr, rsA, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_RK: return launch_decode<EPI_RK>(p, w.R, pr, ldr, rsA, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_EULER: return launch_decode<EPI_EULER>(p, w.R, pr, ldr, rsA, csB, g.a_step, g.b_step, c.nmod, st);
     case EPI_EULER_CORR:
-      return launch_decode<EPI_EULER_CORR>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
-    case EPI_ACCEL: return launch_decode<EPI_ACCEL>(p, w.R, pr, ldr, w.rs, csB, g.a_step, g.b_step, c.nmod, st);
+      return launch_decode<EPI_EULER_CORR>(p, w.R, pr, ldr, rsA, csB, g.a_step, g.b_step, c.nmod, st);
+    case EPI_ACCEL: return launch_decode<EPI_ACCEL>(p, w.R, pr, ldr, rsA, csB, g.a_step, g.b_step, c.nmod, st);
   }
   return cudaErrorInvalidValue;
 }
