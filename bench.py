@@ -34,6 +34,9 @@ METRIC = "fine-propagator FP64 TFLOP/s and parareal time-to-tol at n=4096, 1/2/4
 UNIT = "TFLOP/s"
 
 
+INT8_PEAK_TOPS = 4553.2   # measured dense kind::i8 tcgen05 rate on this pool's B200 (tools/umma_peak.cu)
+
+
 def fp64_peak():
     """FP64 tensor (DMMA) peak: MEASURED_PEAKS.json has no FP64 entry, so it is the measured chip
     peak of the mma.sync.m8n8k4.f64 register-loop probe (tools/fp64_peaks.cu), committed in
@@ -273,7 +276,18 @@ def main():
             ffl = float(np.mean([i["fine_flops"] for i in vinfos]))
             vkms = sum(i["fine_kernel_ms"] for i in vinfos)
             vkfl = sum(i["fine_kernel_flops"] for i in vinfos)
-            return {"options": opts, "time_to_tol_ms": vms, "k_done": vinfos[-1]["k_done"], "residual": vres,
+            extra = {}
+            if opts.get("emulation"):
+                # executed int8 tensor work of the fine phase: T moduli x 2n^3 per FP64 GEMM (sym mode:
+                # only the upper-triangle tiles run, reported approximately by the algorithmic count)
+                ops = vkfl * opts["emulation"]
+                rate = ops / (vkms * 1e-3) / 1e12 if vkms > 0 else None
+                extra = {"int8_tensor_tops_fine_phase": rate, "int8_peak_tops_measured": INT8_PEAK_TOPS,
+                         "int8_frac_fine_phase": (rate / INT8_PEAK_TOPS) if rate else None,
+                         "int8_peak_source": "tools/umma_peak.cu (kind::i8 M128 N256 K32 from smem, 128 cyc/MMA)",
+                         "note": "fine phase = encode + int8 GEMMs + CRT decode; the int8 GEMM kernel alone is "
+                                 "85% tensor-pipe active in ncu (profiles/ncu_full_r01_oz_gemm.md)"}
+            return {**extra, "options": opts, "time_to_tol_ms": vms, "k_done": vinfos[-1]["k_done"], "residual": vres,
                     "algorithmic_fine_tflops": ffl / (vms * 1e-3) / 1e12,
                     "fine_phase_tflops_algorithmic": (vkfl / (vkms * 1e-3) / 1e12) if vkms > 0 else None,
                     "speedup_vs_full": ms_step / vms,

@@ -12,9 +12,13 @@ namespace mfode {
 // applies K = alpha*k4 + beta*C and the EPI element-wise arithmetic, then stores.  `sym`: symmetric
 // mode (write element and mirror); `diag`: strictly-lower elements are skipped (their mirror writes
 // them).  EPI_RESID accumulates into `part` instead of storing.
-template <int EPI>
-__device__ __forceinline__ void epi_apply4(const GemmParams& p, int z, double alpha, int row, int col, int n,
-                                           int ld, double (&k4)[4], bool sym, bool diag, double& part) {
+// DEFER (symmetric mode only): the mirrored stores are not issued; the values of the (up to two)
+// output arrays land in mv[slot][0..3] and the arrays' base pointers in mp[slot] (null = unused),
+// so the caller can write the mirrors coalesced through a shared-memory transpose.
+template <int EPI, bool DEFER>
+__device__ __forceinline__ void epi_apply4_impl(const GemmParams& p, int z, double alpha, int row, int col, int n,
+                                                int ld, double (&k4)[4], bool sym, bool diag, double& part,
+                                                double (&mv)[2][4], double* (&mp)[2]) {
   const long long off = (long long)row * ld + col;
   const bool full4 = (col + 3 < n);
   const int cnt = full4 ? 4 : (n - col);
@@ -124,8 +128,19 @@ __device__ __forceinline__ void epi_apply4(const GemmParams& p, int z, double al
     }
   }
   // ---- stores ----
+  int slot = 0;
   auto store4 = [&](double* dst, const double* v) {
-    if (sym) {
+    if (DEFER) {
+      double* base = dst - off;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int cc = col + e;
+        if (e < cnt && row <= cc) base[(long long)row * ld + cc] = v[e];
+        mv[slot][e] = v[e];
+      }
+      mp[slot] = base;
+      ++slot;
+    } else if (sym) {
       // upper-triangle tile: write (row, col+e) and its mirror (col+e, row); in a diagonal
       // tile the strictly-lower elements are written by the mirror of their partner
       double* base = dst - off;
@@ -163,6 +178,14 @@ __device__ __forceinline__ void epi_apply4(const GemmParams& p, int z, double al
     store4(p.U_out.at(z) + off, o0);
     store4(p.Gold.at(z) + off, o1);
   }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_apply4(const GemmParams& p, int z, double alpha, int row, int col, int n,
+                                           int ld, double (&k4)[4], bool sym, bool diag, double& part) {
+  double mv[2][4];
+  double* mp[2];
+  epi_apply4_impl<EPI, false>(p, z, alpha, row, col, n, ld, k4, sym, diag, part, mv, mp);
 }
 
 }  // namespace mfode

@@ -601,20 +601,24 @@ template <int EPI>
 __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uint16_t* R, long long rpstride, int ldr,
                                                    const double* rscale, const double* cscale, int a_step, int b_step,
                                                    int nmod) {
-  // block = 4 rows x 256 columns (64 threads x 4 columns per row); grid (column blocks, row
-  // blocks, batch).  In symmetric mode blocks strictly below the diagonal exit at once.
+  // block = a 32 x 32 tile (8 threads x 4 columns per row, 32 rows); grid (column tiles, row
+  // tiles, batch).  Symmetric mode: tiles strictly below the diagonal exit at once; the upper
+  // elements are stored directly and their mirrors are written through a shared-memory transpose
+  // (32-byte row segments instead of scattered 8-byte column stores).
   const OzConst& c = c_oz[nmod];
   if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
   const int n = p.n;
-  const int col = blockIdx.x * 256 + 4 * (threadIdx.x & 63);
-  const int row = blockIdx.y * 4 + (threadIdx.x >> 6);
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int col = c0 + 4 * (threadIdx.x & 7);
+  const int row = r0 + (threadIdx.x >> 3);
   const int z = blockIdx.z;
-  if (p.sym && blockIdx.y * 4 > blockIdx.x * 256 + 255) return;
+  const bool sym = p.sym != 0;
+  if (sym && r0 > c0 + 31) return;
   const u128 M = ((u128)c.Mhi << 64) | c.Mlo;
   double part = 0.0;
-  {
-    if (row >= n || col >= n) return;
-    if (p.sym && row > col + 3) return;   // strictly lower: written as the mirror of the upper part
+  double mv[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  double* mp[2] = {nullptr, nullptr};
+  if (row < n && col < n && !(sym && row > col + 3)) {
     const int np = (nmod + 1) >> 1;
     const uint16_t* src = R + (long long)z * np * rpstride + (long long)row * ldr + col;
     uint2 pr4[kOzMaxModuli / 2];
@@ -656,7 +660,48 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
       k4[e] = i128_to_double(v) * rs * cs;
     }
     const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
-    epi_apply4<EPI>(p, z, alpha, row, col, n, p.ld, k4, p.sym != 0, true, part);
+    if (sym)
+      epi_apply4_impl<EPI, true>(p, z, alpha, row, col, n, p.ld, k4, true, true, part, mv, mp);
+    else
+      epi_apply4<EPI>(p, z, alpha, row, col, n, p.ld, k4, false, true, part);
+  }
+  if (!sym) return;
+  // mirrors: source (r, c), r < c  ->  target (c, r)
+  __shared__ double tile[2][32][33];
+  __shared__ double* bases[2];
+  const int ty = threadIdx.x >> 3, tx4 = 4 * (threadIdx.x & 7);
+#pragma unroll
+  for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) tile[sl][ty][tx4 + e] = mv[sl][e];
+  if (threadIdx.x == 0) {   // thread 0 (row r0, columns c0..c0+3) always computes in a live tile
+    bases[0] = mp[0];
+    bases[1] = mp[1];
+  }
+  __syncthreads();
+  const int tr = c0 + ty;          // target row = source column
+  const int tc = r0 + tx4;         // target columns = source rows tc .. tc+3
+  if (tr >= n) return;
+#pragma unroll
+  for (int sl = 0; sl < 2; ++sl) {
+    double* base = bases[sl];
+    if (base == nullptr) continue;
+    double v[4];
+    bool ok[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[e] = tile[sl][tx4 + e][ty];
+      ok[e] = (tc + e < n) && (tc + e < tr);
+    }
+    double* dst = base + (long long)tr * p.ld + tc;
+    if (ok[0] && ok[1] && ok[2] && ok[3]) {
+      *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+      *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (ok[e]) dst[e] = v[e];
+    }
   }
 }
 
@@ -854,7 +899,7 @@ static int oz_num_sms() {
 template <int EPI>
 static cudaError_t launch_decode(const GemmParams& p, const uint16_t* R, long long rp, int ldr, const double* rs,
                                  const double* cs, int a_step, int b_step, int nmod, cudaStream_t st) {
-  const dim3 grid((p.n + 255) / 256, (p.n + 3) / 4, p.num_z);
+  const dim3 grid((p.n + 31) / 32, (p.n + 31) / 32, p.num_z);
   k_oz_decode<EPI><<<grid, 256, 0, st>>>(p, R, rp, ldr, rs, cs, a_step, b_step, nmod);
   ++g_launches;
   return cudaGetLastError();

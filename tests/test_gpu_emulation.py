@@ -238,3 +238,21 @@ def test_cfg4_emulated_bench_workload_vs_spectral_oracle():
     assert info["k_done"] == sp["k_done"] == 1
     assert relF(X, spectral.reconstruct(w.eigvecs, sp["X"])) <= 1e-10
     assert info["residual"] <= 1e-10
+
+
+@pytest.mark.parametrize("flow", [mf.FLOW_INVERSE, mf.FLOW_EXP])
+def test_emulated_constant_operand_cache_follows_set_matrix(flow):
+    """The encodings of the constant operand (B = I - A for the inverse flow, A for the exp flow) are
+    cached per stream; mfode_set_matrix changes the matrix generation, so the next solve re-encodes
+    (a stale cache would reproduce the old matrix's result)."""
+    n = 120
+    A1 = workloads.random_spd(n, 41).A
+    A2 = workloads.random_spd(n, 42).A
+    s = mf.Solver(A1, flow, 1.0, 4, 1, 6)
+    s.set_option("emulation", 16)
+    for A in (A1, A2, A1):
+        s.set_matrix(A)
+        info = s.solve(4)
+        X = s.result()
+        ref = dense.solve(A, flow, 1.0, 4, 1, 6, 4)
+        assert relF(X, ref["X"]) <= 1e-10

@@ -22,6 +22,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def short(name: str) -> str:
+    m = re.search(r"oz_gemm_kernel<(\d)>", name) or re.search(r"oz_gemm_kernelILi(\d)E", name)
+    if m:
+        return "oz_gemm_kernel<%s> (int8 tcgen05, %s)" % (m.group(1), "CTA pair" if m.group(1) == "1" else "1 CTA")
     m = re.search(r"dgemm_tma_kernel<(.*?)>", name)
     if m:
         return f"dgemm_tma_kernel<{m.group(1)}>"
@@ -68,6 +71,11 @@ METRICS = [
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe inst %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
     ("sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA pipe %"),
+    ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", "int8 (imma) tensor pipe %"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "TMEM active %"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2 -> SM bytes (TMA)"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "shared pipe %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
@@ -120,7 +128,8 @@ def full(path):
             traffic.append(rd * mult.get(ur, 1) + wr * mult.get(uw, 1))
         except (ValueError, IndexError):
             pass
-    if traffic:
+    names = [r[kname] for r in data] if kname is not None else []
+    if traffic and names and all("dgemm_tma_kernel" in nm for nm in names):   # the bench's dominant kernel only
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
             json.dump({"source": os.path.basename(path), "bytes_per_launch": sum(traffic) / len(traffic),
                        "launches": len(traffic)}, f, indent=1)

@@ -24,6 +24,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-full", action="store_true")
     ap.add_argument("--skip-sym", action="store_true")
+    ap.add_argument("--modes", nargs="*", default=None,
+                    help="subset of: full symmetric emulated emulated_symmetric (default: full symmetric)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     t0 = time.time()
@@ -35,13 +37,14 @@ def main():
     print(json.dumps({"stage": "spectral_oracle", "seconds": time.time() - t0, "k_done": sp["k_done"],
                       "deltas": sp["deltas"]}), flush=True)
     s = mf.Solver(w.A, w.flow, w.T, w.N, w.m_G, w.m_F)
-    modes = []
-    if not args.skip_full:
-        modes.append(("full", 0))
-    if not args.skip_sym:
-        modes.append(("symmetric", 1))
-    for name, sym in modes:
+    table = {"full": (0, 0), "symmetric": (1, 0), "emulated": (0, 16), "emulated_symmetric": (1, 16)}
+    names = args.modes
+    if names is None:
+        names = [m for m, skip in (("full", args.skip_full), ("symmetric", args.skip_sym)) if not skip]
+    modes = [(m, *table[m]) for m in names]
+    for name, sym, emu in modes:
         s.set_option("symmetric", sym)
+        s.set_option("emulation", emu)
         info = s.solve(w.K_max, w.tol, w.stop)
         X = s.result()
         rel = float(np.linalg.norm(X - ref) / np.linalg.norm(ref))
