@@ -51,12 +51,8 @@ struct OzConst {
   int nmod;
   int abits;                           // operands are scaled to integers of magnitude <= 2^abits
   uint32_t m[kOzMaxModuli];            // moduli
-  double minv[kOzMaxModuli];           // 1 / m
-  unsigned long long wlo[kOzMaxModuli], whi[kOzMaxModuli];   // CRT weights w_t (128-bit)
-  double wf[kOzMaxModuli];             // w_t / M
   unsigned long long Mlo, Mhi;         // M = prod m_t (128-bit)
   uint32_t pw[kOzMaxModuli / 2][4];    // CRT weights of the pair groups (m_2i m_2i+1), 32-bit limbs
-  double pwf[kOzMaxModuli / 2];        // pair weight / M
   uint32_t pwq[kOzMaxModuli / 2];      // pair weight / M in 0.32 fixed point (decode quotient)
   uint32_t pinv[kOzMaxModuli / 2];     // m_2i^-1 mod m_2i+1 (epilogue pair CRT)
 };

@@ -78,18 +78,10 @@ bool oz_make_const(int nmod, int k, OzConst* c) {
   if (c->abits < 8) return false;
   c->Mlo = (unsigned long long)M;
   c->Mhi = (unsigned long long)(M >> 64);
-  for (int t = 0; t < nmod; ++t) {
-    const uint32_t m = kOzModuli[t];
-    const u128 Mt = M / m;
-    const uint32_t inv = modinv_small((uint32_t)(Mt % m), m);
-    const u128 w = Mt * inv;   // < M: w = 1 mod m_t, 0 mod the others
-    c->m[t] = m;
-    c->minv[t] = 1.0 / (double)m;
-    c->wlo[t] = (unsigned long long)w;
-    c->whi[t] = (unsigned long long)(w >> 64);
-    c->wf[t] = (double)((long double)w / (long double)M);
-  }
-  // the decode combines residues in pairs (m_2i, m_2i+1) first; a lone last modulus forms its own group
+  for (int t = 0; t < nmod; ++t) c->m[t] = kOzModuli[t];
+  // CRT over the pair groups P_i = m_2i m_2i+1 (a lone last modulus forms its own group): the GEMM
+  // epilogue combines each pair, the decode combines the groups with weights W_i = (M/P_i) *
+  // ((M/P_i)^-1 mod P_i) < M (W_i = 1 mod P_i, 0 mod the other groups)
   for (int i = 0; 2 * i < nmod; ++i) {
     const uint32_t P = kOzModuli[2 * i] * (2 * i + 1 < nmod ? kOzModuli[2 * i + 1] : 1u);
     const u128 Mi = M / P;
@@ -97,7 +89,6 @@ bool oz_make_const(int nmod, int k, OzConst* c) {
     const u128 w = Mi * inv;
     for (int j = 0; j < 4; ++j) c->pw[i][j] = (uint32_t)(w >> (32 * j));
     c->pinv[i] = (2 * i + 1 < nmod) ? modinv_small(kOzModuli[2 * i] % kOzModuli[2 * i + 1], kOzModuli[2 * i + 1]) : 0u;
-    c->pwf[i] = (double)((long double)w / (long double)M);
     c->pwq[i] = (uint32_t)std::floor((long double)w / (long double)M * 4294967296.0L);   // w/M in 0.32 fixed point
   }
   return true;

@@ -256,3 +256,41 @@ def test_emulated_constant_operand_cache_follows_set_matrix(flow):
         X = s.result()
         ref = dense.solve(A, flow, 1.0, 4, 1, 6, 4)
         assert relF(X, ref["X"]) <= 1e-10
+
+
+@pytest.mark.parametrize("flow,n", [(mf.FLOW_EXP, 140), (mf.FLOW_TRIG, 72)])
+def test_emulated_modified_parareal_vs_oracle(flow, n):
+    """f2 (Algorithm 3) on the emulated GEMMs: same bar as the DMMA path's test."""
+    w = workloads.random_spd(n, 12, lo=0.5, hi=3.0)
+    N, mG, mF, K = 10, 1, 10, 3
+    s = mf.Solver(w.A, flow, 1.0, N, mG, mF)
+    s.set_option("emulation", 16)
+    info = s.solve_modified(K)
+    rows = 2 * n if flow == mf.FLOW_TRIG else n
+    X = np.empty((rows, n))
+    s.result(X)
+    ref = dense.solve_modified(w.A, flow, 1.0, N, mG, mF, K)
+    seq = dense.solve_sequential_fine(w.A, flow, 1.0, N, mF)
+    assert info["k_done"] == K
+    err_gpu = relF(X, seq)
+    err_ref = relF(ref["X"], seq)
+    assert relF(X, ref["X"]) <= 1e-10 or (err_gpu <= 1e-10 and err_ref <= 1e-10)
+
+
+@pytest.mark.parametrize("n", [100, 300, 4096])
+def test_single_cta_and_pair_kernels_bitwise_equal(n):
+    """The single-CTA (oz_pair = 0) and CTA-pair (default) int8 GEMM kernels compute the same exact
+    integer products, so the emulated results are bitwise identical."""
+    rng = np.random.default_rng(77 + n)
+    A = rng.standard_normal((n, n))
+    B = rng.standard_normal((n, n))
+    knob = mf.Solver(np.eye(2), mf.FLOW_INVERSE, 1.0, 1, 1, 1)
+    try:
+        knob.set_option("oz_pair", 0)
+        D0 = mf.dgemm_emulated(_dev(A), _dev(B)).cpu().numpy()
+    finally:
+        knob.set_option("oz_pair", 1)
+    D1 = mf.dgemm_emulated(_dev(A), _dev(B)).cpu().numpy()
+    assert np.array_equal(D0, D1)
+    if n <= 300:
+        assert np.all(np.abs(D1 - A @ B) <= emu_bound(A, B, abits(16, n)))
