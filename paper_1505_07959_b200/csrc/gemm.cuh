@@ -262,9 +262,13 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
           }
         }
         if (kb == 1) {
-          // Every shared-memory read of this stage is issued: release it to the producer now
-          // (the arrive has release semantics), and probe the next stage's full barrier so the
-          // probe's latency hides behind this k-step's DMMAs instead of stalling the next one.
+          // Every shared-memory read of this stage is issued: release it to the producer now,
+          // and probe the next stage's full barrier so the probe's latency hides behind this
+          // k-step's DMMAs instead of stalling the next one.  The producer refills the stage
+          // with TMA (async proxy), so the generic-proxy reads must be ordered before it by a
+          // proxy fence: without it a still-pending ld.shared could observe the refill (seen as
+          // rare wrong 32 x 16 warp sub-tiles when the producer waits at the stage).
+          fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[stage]);
           const int ns = (stage + 1 == STAGES) ? 0 : stage + 1;

@@ -456,3 +456,29 @@ def test_small_kernels_logical_ranks_and_sequential():
     XN = s1.result()
     s1.sequential_fine()
     assert np.array_equal(s1.result(), XN)     # P5 on the K6 path
+
+
+def test_symmetric_mode_repeatable_inverse_n2048():
+    """Regression (round 1): the DMMA consumers read each TMA-filled shared-memory stage with
+    generic-proxy loads and released it early to the producer; without a proxy fence the TMA
+    refill could overtake a pending load, corrupting one warp's 32 x 16 sub-tile in ~1-3 % of
+    symmetric-mode launches (long mirrored epilogues made the producer wait at the stage).
+    Repeated symmetric solves of the inverse flow at n = 2048 (TILE_64) must agree bitwise and
+    match the full-product result at rounding level."""
+    n = 2048
+    rng = np.random.default_rng(3)
+    G = rng.standard_normal((n, n))
+    A = np.eye(n) + (G.T @ G) / (2 * n)
+    A = (A + A.T) / 2
+    s = mf.Solver(A, mf.FLOW_INVERSE, 1.0, 4, 1, 4)
+    s.set_option("tile", 2)
+    s.solve(2)
+    ref = s.result()
+    s.set_option("symmetric", 1)
+    outs = []
+    for _ in range(6):
+        s.solve(2)
+        outs.append(s.result())
+    for X in outs:
+        assert np.array_equal(X, outs[0])
+    assert relF(outs[0], ref) <= 1e-13
