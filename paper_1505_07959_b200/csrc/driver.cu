@@ -374,7 +374,7 @@ static int fine_chunk_size(const mfode_ctx* h, int active) {
   if (h->small || active <= 1) return std::max(1, std::min(active, h->cap));
   const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, std::min(active, h->cap), h->sym);
   const long long t1 = gemm_tiles(tile, h->n, 1, h->sym) * h->ms;   // tiles of one slice's GEMM launch
-  const long long slots = 148LL * (tile == TILE_128 ? 1 : ((tile == TILE_64 || tile == TILE_128x64) ? 2 : 4));
+  const long long slots = 148LL * (tile == TILE_128 ? 1 : (tile == TILE_64 ? 2 : 4));
   const long long launches = (long long)h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
   const long long euler_gemms = (long long)h->mG * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
   const long long coarse_rounds = (t1 + slots - 1) / slots;
@@ -1358,7 +1358,7 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     return MFODE_OK;
   }
   if (!strcmp(key, "tile")) {
-    if (value < 0 || value > 4) return fail(h, MFODE_EINVAL, "tile must be 0..4");
+    if (value < 0 || value > 3) return fail(h, MFODE_EINVAL, "tile must be 0..3");
     h->tile = (int)value;
     return MFODE_OK;
   }
@@ -1410,7 +1410,7 @@ void mfode_destroy(mfode_ctx* h) {
 int mfode_dgemm(const double* dA, const double* dB, const double* dC, double* dD, int64_t n, int64_t ld, double alpha,
                 double beta, int tile, void* stream) {
   if (!dA || !dB || !dD || (beta != 0.0 && !dC)) return set_global_err(MFODE_EINVAL, "NULL argument");
-  if (n < 1 || ld < n || (ld * 8) % 16 != 0 || tile < 0 || tile > 4)
+  if (n < 1 || ld < n || (ld * 8) % 16 != 0 || tile < 0 || tile > 3)
     return set_global_err(MFODE_EINVAL, "bad n/ld/tile");
   GemmParams p;
   memset(&p, 0, sizeof(p));
@@ -1461,7 +1461,7 @@ int mfode_rk_stage(const double* dYop, const double* dBop, const double* dC, dou
                    double* dS, double* dYnext, int stage, double h, int64_t n, int64_t ld, int tile, void* stream) {
   if (!dYop || !dBop || !dX || !dS || (stage < 4 && !dYnext) || (beta != 0.0 && !dC))
     return set_global_err(MFODE_EINVAL, "NULL argument");
-  if (stage < 1 || stage > 4 || n < 1 || ld < n || (ld * 8) % 16 != 0 || tile < 0 || tile > 4)
+  if (stage < 1 || stage > 4 || n < 1 || ld < n || (ld * 8) % 16 != 0 || tile < 0 || tile > 3)
     return set_global_err(MFODE_EINVAL, "bad stage/n/ld/tile");
   GemmParams p;
   memset(&p, 0, sizeof(p));

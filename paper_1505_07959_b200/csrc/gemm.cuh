@@ -82,9 +82,6 @@ struct GemmCfg {
   static constexpr bool kSetMaxNReg = (kConsumerWarps % 4 == 0) && (kConsumerWarps >= 8);
   static constexpr int kProducerWarps = kSetMaxNReg ? 4 : 1;
   static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
-  // CTAs per SM the launch bounds ask for: the 8-consumer-warp config owns the SM; the smaller
-  // ones run two CTAs per SM so one CTA's epilogue overlaps the other's main loop
-  static constexpr int kMinBlocks = kSetMaxNReg ? 1 : 2;
   static constexpr int WM = BM / WARPS_M;
   static constexpr int WN = BN / WARPS_N;
   static constexpr int MT = WM / 8;          // 8-row m-tiles per warp
@@ -115,8 +112,7 @@ __device__ __forceinline__ void tile_coords(bool sym, int r, int tiles_n, int& t
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int EPI>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads,
-                                  GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmParams p) {
   using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>;

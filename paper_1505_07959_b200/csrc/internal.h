@@ -9,7 +9,7 @@
 
 namespace mfode {
 
-enum Tile : int { TILE_AUTO = 0, TILE_128 = 1, TILE_64 = 2, TILE_32 = 3, TILE_128x64 = 4 };
+enum Tile : int { TILE_AUTO = 0, TILE_128 = 1, TILE_64 = 2, TILE_32 = 3 };
 
 // A GEMM operand: matrix `base + z * step` of a slab of `count` n x n matrices at `slab`.
 struct Operand {

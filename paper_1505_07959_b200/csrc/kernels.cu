@@ -442,7 +442,7 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
   return e;
 }
 
-int tile_box_rows(int tile) { return (tile == TILE_128 || tile == TILE_128x64) ? 128 : (tile == TILE_64 ? 64 : 32); }
+int tile_box_rows(int tile) { return tile == TILE_128 ? 128 : (tile == TILE_64 ? 64 : 32); }
 
 int choose_tile(int n, int num_z, bool sym) {
   auto tiles = [&](int bm, int bn) {
@@ -457,7 +457,6 @@ int choose_tile(int n, int num_z, bool sym) {
 
 long long gemm_tiles(int tile, int n, int num_z, bool sym) {
   const int bm = tile_box_rows(tile), bn = (tile == TILE_128) ? 128 : 64;
-  if (tile == TILE_128x64) sym = false;   // rectangular tiles: symmetric mode computes every tile
   const long long tm = (n + bm - 1) / bm;
   return ((sym && bm == bn) ? tm * (tm + 1) / 2 : tm * ((n + bn - 1) / bn)) * num_z;
 }
@@ -468,7 +467,6 @@ static cudaError_t dispatch_tile(int tile, const CUtensorMap& ma, const CUtensor
   switch (tile) {
     case TILE_128: return launch_cfg<128, 128, 2, 4, 4, EPI>(ma, mb, p, st);
     case TILE_64: return launch_cfg<64, 64, 2, 2, 4, EPI>(ma, mb, p, st);
-    case TILE_128x64: return launch_cfg<128, 64, 2, 2, 4, EPI>(ma, mb, p, st);
     default: return launch_cfg<32, 64, 1, 2, 4, EPI>(ma, mb, p, st);
   }
 }

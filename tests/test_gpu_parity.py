@@ -45,7 +45,7 @@ def relF(x, ref):
 # ---------------------------------------------------------------------------------------------
 # kernel level
 # ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("tile", [1, 2, 3, 4])
+@pytest.mark.parametrize("tile", [1, 2, 3])
 @pytest.mark.parametrize("n", [1, 8, 30, 64, 100, 129, 256, 500])
 def test_dgemm_parity(n, tile):
     rng = np.random.default_rng(n * 10 + tile)
@@ -87,15 +87,14 @@ def test_dgemm_large_sampled():
     assert np.linalg.norm(got - ref) <= bound
 
 
-@pytest.mark.parametrize("tile", [0, 4])
 @pytest.mark.parametrize("stage", [1, 2, 3, 4])
 @pytest.mark.parametrize("n", [40, 256])
-def test_rk_stage_parity(n, stage, tile):
+def test_rk_stage_parity(n, stage):
     rng = np.random.default_rng(stage)
     Y, W, X, S = (rng.standard_normal((n, n)) for _ in range(4))
     h = 1.0 / 64
     dX, dS, dYn = _dev(X), _dev(S), _dev(np.zeros((n, n)))
-    mf.rk_stage(_dev(Y), _dev(W), dX, dS, dYn, stage, h, tile=tile)
+    mf.rk_stage(_dev(Y), _dev(W), dX, dS, dYn, stage, h)
     K = Y @ W
     tolK = 2 * n * U53 * np.abs(Y) @ np.abs(W)
     if stage == 4:
