@@ -70,6 +70,13 @@ def test_create_rejects_bad_arguments_without_gpu():
     assert b"world" in L.mfode_last_global_error()
     assert L.mfode_parareal_solve(None, 1, 0.0, 0, None) == mf.EINVAL
     assert L.mfode_dgemm(None, None, None, None, 4, 4, 1.0, 0.0, 0, None) == mf.EINVAL
+    # f3(ii) emulated GEMM: NULL operands, moduli count and size limits are checked before any CUDA call
+    x = ctypes.c_void_p(1)
+    assert L.mfode_dgemm_emulated(None, None, None, None, 4, 4, 1.0, 0.0, 16, None) == mf.EINVAL
+    assert L.mfode_dgemm_emulated(x, x, None, x, 4, 4, 1.0, 0.0, 1, None) == mf.EINVAL
+    assert L.mfode_dgemm_emulated(x, x, None, x, 4, 4, 1.0, 0.0, 17, None) == mf.EINVAL
+    assert L.mfode_dgemm_emulated(x, x, None, x, 40000, 40000, 1.0, 0.0, 16, None) == mf.EINVAL
+    assert L.mfode_dgemm_emulated(x, x, None, x, 4, 3, 1.0, 0.0, 16, None) == mf.EINVAL
 
 
 def test_no_oracle_import_in_product_path():
