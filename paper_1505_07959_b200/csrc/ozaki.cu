@@ -589,7 +589,7 @@ __device__ __forceinline__ double i128_to_double(i128 v) {   // correctly rounde
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uint16_t* R, long long rpstride, int ldr,
+__global__ void __launch_bounds__(256, 4) k_oz_decode(const GemmParams p, const uint16_t* R, long long rpstride, int ldr,
                                                    const double* rscale, const double* cscale, int a_step, int b_step,
                                                    int nmod) {
   // block = a 32 x 32 tile (8 threads x 4 columns per row, 32 rows); grid (column tiles, row
@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(256) k_oz_decode(const GemmParams p, const uin
   if (row < n && col < n && !(sym && row > col + 3)) {
     const int np = (nmod + 1) >> 1;
     const uint16_t* src = R + (long long)z * np * rpstride + (long long)row * ldr + col;
+    }
     uint2 pr4[kOzMaxModuli / 2];
 #pragma unroll
     for (int i = 0; i < kOzMaxModuli / 2; ++i)
