@@ -612,7 +612,6 @@ __global__ void __launch_bounds__(256, 4) k_oz_decode(const GemmParams p, const 
   if (row < n && col < n && !(sym && row > col + 3)) {
     const int np = (nmod + 1) >> 1;
     const uint16_t* src = R + (long long)z * np * rpstride + (long long)row * ldr + col;
-    }
     uint2 pr4[kOzMaxModuli / 2];
 #pragma unroll
     for (int i = 0; i < kOzMaxModuli / 2; ++i)
