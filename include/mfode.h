@@ -32,7 +32,8 @@
  * ncclGetUniqueId broadcast by the caller) or, with dist->nccl_uid == NULL and dist->world > 1,
  * between LOGICAL ranks inside one process on one device (same partition, same kernels, boundary
  * copies by cudaMemcpyAsync; used to check P-invariance on one GPU).  In NCCL mode every rank
- * calls every function collectively.
+ * calls every function collectively.  A non-NULL nccl_uid with world == 1 creates a one-rank
+ * communicator (the NCCL code path -- metric and result broadcasts -- on a single GPU).
  */
 #ifndef MFODE_H
 #define MFODE_H

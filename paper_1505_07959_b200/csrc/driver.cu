@@ -690,7 +690,7 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   else cudaGetDevice(&dev);
   h->device = dev;
   if (cudaSetDevice(dev) != cudaSuccess) return set_global_err(MFODE_ECUDA, "cudaSetDevice(%d) failed", dev);
-  h->nccl_mode = dist && dist->nccl_uid && world > 1;
+  h->nccl_mode = dist && dist->nccl_uid;   // world == 1 is a one-rank communicator (same code path)
   if (h->nccl_mode) {
     if (dist->rank < 0 || dist->rank >= world) return set_global_err(MFODE_EINVAL, "rank out of range");
     h->my_rank = dist->rank;

@@ -62,3 +62,39 @@ def test_nccl_two_ranks_bitwise():
         assert p.exitcode == 0
     assert k == i1["k_done"]
     assert np.array_equal(X, X1)
+
+
+def test_nccl_one_rank_communicator_bitwise():
+    """NCCL mode with a one-rank communicator (runs on a single GPU): the NCCL code path (metric
+    broadcasts, stop-flag copies, result broadcast) gives bitwise the result of the default mode,
+    including speculative overlap with a tolerance stop and the sqrt flow's residual stop."""
+    import paper_1505_07959_b200 as mf
+    import workloads
+    w = workloads.random_spd(96, 5)
+    for flow, T, N, mG, mF, K, tol, stop in ((mf.FLOW_INVERSE, 1.0, 8, 1, 8, 8, 1e-12, mf.STOP_DELTA),
+                                             (mf.FLOW_INVERSE, 1.0, 6, 1, 4, 3, 0.0, mf.STOP_FIXED_K)):
+        s = mf.Solver(w.A, flow, T, N, mG, mF)
+        i1 = s.solve(K, tol, stop)
+        X1 = s.result()
+        s.close()
+        uid = bytes(torch.cuda.nccl.unique_id())   # one unique id per communicator (one-shot bootstrap)
+        s = mf.Solver(w.A, flow, T, N, mG, mF, world=1, rank=0, device=0, nccl_uid=uid)
+        i2 = s.solve(K, tol, stop)
+        X2 = s.result()
+        s.close()
+        assert i1["k_done"] == i2["k_done"]
+        assert np.array_equal(X1, X2)
+    m = 8
+    import numpy as _np
+    A = workloads.laplacian_2d(m) + _np.eye(m * m)
+    s = mf.Solver(A, mf.FLOW_SQRT, 20.0, 64, 2, 16)
+    i1 = s.solve(4, 1e-10, mf.STOP_RESIDUAL)
+    X1 = s.result()
+    s.close()
+    s = mf.Solver(A, mf.FLOW_SQRT, 20.0, 64, 2, 16, world=1, rank=0, device=0,
+                  nccl_uid=bytes(torch.cuda.nccl.unique_id()))
+    i2 = s.solve(4, 1e-10, mf.STOP_RESIDUAL)
+    X2 = s.result()
+    s.close()
+    assert i1["k_done"] == i2["k_done"]
+    assert np.array_equal(X1, X2)
