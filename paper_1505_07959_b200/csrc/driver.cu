@@ -246,6 +246,7 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     Operand Wop{Wbuf, Wcount, 0, 1};
     p.alpha = 1.0;
     p.beta = 0.0;
+    p.oz_reuse_left = 1;   // Y was the right operand of the launch just above and is unchanged
     CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Wop, p, st));
   } else if (h->flow == MFODE_FLOW_SQRT) {
     if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));

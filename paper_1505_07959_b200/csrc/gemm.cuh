@@ -63,6 +63,7 @@ struct GemmParams {
   double shift;           // EPI_RESID: subtract shift * I
   double* partials;       // EPI_RESID: one double per tile (index z * tiles + tile)
   const int* stop_flag;   // if non-null and set: the launch does nothing
+  int oz_reuse_left;      // emulated GEMM: A == the previous launch's right operand, unchanged (ozaki.cu)
   int oz_nmod;            // > 0: emulated FP64 GEMM on the int8 tensor cores with this many moduli (ozaki.cu)
 };
 

@@ -709,8 +709,16 @@ struct OzCached {
   double* scale;
 };
 
+// identity of the right operand last row-encoded (symmetric mode) into OzWork::B / cs
+struct OzLastB {
+  const double* slab = nullptr;
+  int base = 0, step = 0, nenc = 0, n = 0, ld = 0, nmod = 0;
+  bool valid = false;
+};
+
 struct OzWork {
   std::vector<OzCached> cached;
+  OzLastB lastB;
   uint8_t* A = nullptr;
   uint8_t* B = nullptr;
   uint16_t* R = nullptr;   // pair residues
@@ -945,11 +953,22 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
   const int ldk = oz_ldk(n), ldr = oz_ldr(n);
   const long long pk = (long long)n * ldk, pr = (long long)n * ldr;
   const long long mst = (long long)n * p.ld;
-  // A: row-scaled planes (a constant operand's encoding is cached per stream)
+  // A: row-scaled planes (a constant operand's encoding is cached per stream).  With
+  // p.oz_reuse_left the caller guarantees A is unchanged since the previous launch on this stream,
+  // whose right operand it was: in symmetric mode that row encoding is reused (buffers swapped).
+  const bool reuseA = p.oz_reuse_left && p.sym && w.lastB.valid && w.lastB.slab == A.slab &&
+                      w.lastB.base == A.base && w.lastB.step == A.step && w.lastB.nenc == nA && w.lastB.n == n &&
+                      w.lastB.ld == p.ld && w.lastB.nmod == c.nmod;
+  if (reuseA) {
+    std::swap(w.A, w.B);
+    std::swap(w.capA, w.capB);
+    std::swap(w.rs, w.cs);
+  }
+  w.lastB.valid = false;
   uint8_t* planesA = w.A;
   double* rsA = w.rs;
-  bool encA = true;
-  if (A.step == 0 && A.cache_key != 0) {
+  bool encA = !reuseA;
+  if (!reuseA && A.step == 0 && A.cache_key != 0) {
     if ((e = oz_cache_get(st, A.slab + (size_t)A.base * mst, A.cache_key, 0, c.nmod, n, p.ld, &planesA, &rsA, &encA)) !=
         cudaSuccess)
       return e;
@@ -983,6 +1002,16 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
       k_oz_enc_rows<<<dim3(n, nB), kEncThreads, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, pb, pk, ldk, cb, c.nmod,
                                                          c.abits, flagB);
       ++g_launches;
+      if (pb == w.B) {
+        w.lastB.slab = B.slab;
+        w.lastB.base = B.base;
+        w.lastB.step = B.step;
+        w.lastB.nenc = nB;
+        w.lastB.n = n;
+        w.lastB.ld = p.ld;
+        w.lastB.nmod = c.nmod;
+        w.lastB.valid = true;
+      }
     } else if (encB) {
       if ((e = cudaMemsetAsync(w.ce, 0x80, (size_t)n * nB * sizeof(int), st)) != cudaSuccess) return e;
       k_oz_colexp<<<dim3((n + 31) / 32, (n + 255) / 256, nB), 256, 0, st>>>(B.slab, mst, B.base, B.step, n, p.ld, w.ce,
@@ -994,6 +1023,17 @@ cudaError_t launch_gemm_oz(int epi, const Operand& A, const Operand& B, GemmPara
     }
     planesB = pb;
     csB = cb;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_oz_mu);
+    OzWork& stored = oz_works()[st];
+    stored.A = w.A;
+    stored.B = w.B;
+    stored.capA = w.capA;
+    stored.capB = w.capB;
+    stored.rs = w.rs;
+    stored.cs = w.cs;
+    stored.lastB = w.lastB;
   }
   // integer GEMMs (pair-combined 16-bit residues)
   const bool pair = g_oz_pair;

@@ -294,3 +294,21 @@ def test_single_cta_and_pair_kernels_bitwise_equal(n):
     assert np.array_equal(D0, D1)
     if n <= 300:
         assert np.all(np.abs(D1 - A @ B) <= emu_bound(A, B, abits(16, n)))
+
+
+def test_emulated_symmetric_inverse_reuses_encoding():
+    """Inverse flow, f3(i) + f3(ii): the second GEMM of each stage (K = Y W) reuses the row
+    encoding of Y made for the first (W = B Y); results match the oracle and the non-symmetric
+    emulated run, and repeated solves are bitwise identical."""
+    A = workloads.random_spd(300, 77).A
+    T, N, mG, mF, K = 1.0, 6, 1, 8, 6
+    s, i1, X1 = _solve(A, mf.FLOW_INVERSE, T, N, mG, mF, K, 1e-11, mf.STOP_DELTA, symmetric=1)
+    info2 = s.solve(K, 1e-11, mf.STOP_DELTA)
+    X2 = np.empty_like(X1)
+    s.result(X2)
+    assert np.array_equal(X1, X2) and info2["k_done"] == i1["k_done"]
+    ref = dense.solve(A, mf.FLOW_INVERSE, T, N, mG, mF, K, 1e-11, mf.STOP_DELTA)
+    assert i1["k_done"] == ref["k_done"]
+    assert relF(X1, ref["X"]) <= 1e-10
+    _, _, X3 = _solve(A, mf.FLOW_INVERSE, T, N, mG, mF, K, 1e-11, mf.STOP_DELTA)
+    assert relF(X1, X3) <= 1e-13
