@@ -175,13 +175,21 @@ __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab,
   double mx = 0.0;
   bool bad = false;
   for (int k = 4 * threadIdx.x; k < n; k += 4 * kEncThreads) {
+    double v[4];
+    if (k + 3 < n) {   // rows start 16-byte aligned (ld is a multiple of 2) and k is a multiple of 4
+      const double2 a = *reinterpret_cast<const double2*>(src + k);
+      const double2 b = *reinterpret_cast<const double2*>(src + k + 2);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (k + e < n) {
-        const double v = fabs(src[k + e]);
-        bad |= !(v <= 1.7976931348623157e308);
-        mx = fmax(mx, v);
-      }
+      for (int e = 0; e < 4; ++e) v[e] = (k + e < n) ? src[k + e] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double av = fabs(v[e]);
+      bad |= !(av <= 1.7976931348623157e308);
+      mx = fmax(mx, av);
+    }
   }
   if (bad) bad_s = 1;
 #pragma unroll
@@ -195,10 +203,20 @@ __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab,
   const double scale = ldexp(1.0, abits - e);
   if (threadIdx.x == 0) rscale[(long long)z * n + row] = bad_s ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, e - abits);
   uint8_t* dst = planes + (long long)z * nmod * pstride + (long long)row * ldk;
+#pragma unroll 2
   for (int k = 4 * threadIdx.x; k < ldk; k += 4 * kEncThreads) {
+    double v[4];
+    if (k + 3 < n) {
+      const double2 a = *reinterpret_cast<const double2*>(src + k);
+      const double2 b = *reinterpret_cast<const double2*>(src + k + 2);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (k + q < n) ? src[k + q] : 0.0;
+    }
     long long x[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) x[q] = (k + q < n && !bad_s) ? __double2ll_rn(src[k + q] * scale) : 0LL;
+    for (int q = 0; q < 4; ++q) x[q] = bad_s ? 0LL : __double2ll_rn(v[q] * scale);
     oz_write_residues4(dst + k, pstride, x, nmod);
   }
 }
