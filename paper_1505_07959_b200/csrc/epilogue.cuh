@@ -180,6 +180,29 @@ __device__ __forceinline__ void epi_apply4_impl(const GemmParams& p, int z, doub
   }
 }
 
+// The output arrays epi_apply4_impl<EPI, true> reports in mv / mp, in the same slot order.
+template <int EPI>
+__device__ __forceinline__ void epi_out_ptrs(const GemmParams& p, int z, double* (&mp)[2]) {
+  mp[0] = mp[1] = nullptr;
+  if constexpr (EPI == EPI_STORE) {
+    mp[0] = p.Y_out.at(z);
+  } else if constexpr (EPI == EPI_RK) {
+    if (p.stage == 4) {
+      mp[0] = p.X_out.at(z);
+      if (p.Y_out.p) mp[1] = p.Y_out.at(z);
+    } else {
+      mp[0] = p.S.at(z);
+      mp[1] = p.Y_out.at(z);
+    }
+  } else if constexpr (EPI == EPI_EULER || EPI == EPI_ACCEL) {
+    mp[0] = p.X_out.at(z);
+    if (p.Gold.p) mp[1] = p.Gold.at(z);
+  } else if constexpr (EPI == EPI_EULER_CORR) {
+    mp[0] = p.U_out.at(z);
+    mp[1] = p.Gold.at(z);
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epi_apply4(const GemmParams& p, int z, double alpha, int row, int col, int n,
                                            int ld, double (&k4)[4], bool sym, bool diag, double& part) {

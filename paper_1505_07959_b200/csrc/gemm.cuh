@@ -90,7 +90,12 @@ struct GemmCfg {
   static constexpr int kABytes = BM * BK * 8;
   static constexpr int kBBytes = BN * BK * 8;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8;
+  // symmetric mode: per consumer warp, an 8-row x 32-column staging block (x 2 output arrays) through
+  // which the mirrored elements are written as 64-byte row segments
+  static constexpr int kMirrorPitch = 33;
+  static constexpr int kMirrorDoubles = (BM == BN) ? kConsumerWarps * 2 * 8 * kMirrorPitch : 0;
+  static constexpr int kSmemBytes =
+      STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8 + kMirrorDoubles * 8;
   static_assert(WM % 8 == 0 && WN % 16 == 0, "warp tile must be a multiple of 8 x 16");
   static_assert(BM <= 256 && BN % 16 == 0, "TMA box limits");
 };
@@ -123,6 +128,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
   uint64_t* empty = full + STAGES;
   double* red = reinterpret_cast<double*>(empty + STAGES);   // EPI_RESID cross-warp scratch
+  double* mirror_stage = red + 64;                            // symmetric-mode mirror staging
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -293,6 +299,61 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     // ---------------- epilogue ----------------
     double part = 0.0;
     const int ld = p.ld;
+    if constexpr (EPI != EPI_RESID && BM == BN) {
+      if (sym) {
+        // symmetric mode: direct (upper) stores in the epilogue; the mirrors go through a per-warp
+        // 8 x 32 staging block so that each lane writes 8 consecutive doubles of one target row
+        double* stg = mirror_stage + warp * (2 * 8 * Cfg::kMirrorPitch);
+        double* outp[2];
+        epi_out_ptrs<EPI>(p, z, outp);
+#pragma unroll
+        for (int mt = 0; mt < Cfg::MT; ++mt) {
+          const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
+#pragma unroll
+          for (int ng = 0; ng < Cfg::NG; ++ng) {
+            const int cl = ng * 16 + 4 * c;
+            const int col = n0 + wn * Cfg::WN + cl;
+            double mv[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+            double* mp[2];
+            if (row < n && col < n) {
+              double k4[4] = {acc[mt][2 * ng][0], acc[mt][2 * ng + 1][0], acc[mt][2 * ng][1], acc[mt][2 * ng + 1][1]};
+              epi_apply4_impl<EPI, true>(p, z, alpha, row, col, n, ld, k4, true, m0 == n0, part, mv, mp);
+            }
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) stg[sl * 8 * Cfg::kMirrorPitch + rowA * Cfg::kMirrorPitch + cl + e] = mv[sl][e];
+          }
+          __syncwarp();
+          const int tr = n0 + wn * Cfg::WN + lane;        // target row = source column
+          const int tc0 = m0 + wm * Cfg::WM + mt * 8;     // target columns = the 8 source rows
+          if (tr < n) {
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+              if (outp[sl] == nullptr) continue;
+              double v[8];
+              bool all = true;
+#pragma unroll
+              for (int r = 0; r < 8; ++r) {
+                v[r] = stg[sl * 8 * Cfg::kMirrorPitch + r * Cfg::kMirrorPitch + lane];
+                all = all && (tc0 + r < n) && (tc0 + r < tr);
+              }
+              double* dst = outp[sl] + (long long)tr * ld + tc0;
+              if (all) {
+#pragma unroll
+                for (int r = 0; r < 8; r += 2) *reinterpret_cast<double2*>(dst + r) = make_double2(v[r], v[r + 1]);
+              } else {
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                  if ((tc0 + r < n) && (tc0 + r < tr)) dst[r] = v[r];
+              }
+            }
+          }
+          __syncwarp();
+        }
+        continue;
+      }
+    }
 #pragma unroll
     for (int mt = 0; mt < Cfg::MT; ++mt) {
       const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
