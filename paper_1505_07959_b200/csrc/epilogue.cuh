@@ -12,18 +12,60 @@ namespace mfode {
 // applies K = alpha*k4 + beta*C and the EPI element-wise arithmetic, then stores.  `sym`: symmetric
 // mode (write element and mirror); `diag`: strictly-lower elements are skipped (their mirror writes
 // them).  EPI_RESID accumulates into `part` instead of storing.
+// Epilogue operands of one 4-column group, loaded ahead of the arithmetic (software pipelining of
+// the DMMA epilogue: the loads of group g+1 are in flight while group g is computed and stored).
+struct EpiIn {
+  double c[4], x[4], s[4], f[4];
+};
+
+__device__ __forceinline__ void epi_ld4(const double* src, bool full4, int cnt, double (&v)[4]) {
+  if (full4) {
+    const double2 a0 = *reinterpret_cast<const double2*>(src);
+    const double2 a1 = *reinterpret_cast<const double2*>(src + 2);
+    v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = (e < cnt) ? src[e] : 0.0;
+  }
+}
+
+// Loads exactly the operands epi_apply4_impl<EPI> reads for (row, col .. col+3).
+template <int EPI>
+__device__ __forceinline__ void epi_load4(const GemmParams& p, int z, int row, int col, int n, int ld, EpiIn& in) {
+  const long long off = (long long)row * ld + col;
+  const bool full4 = (col + 3 < n);
+  const int cnt = full4 ? 4 : (n - col);
+  if (p.beta != 0.0) epi_ld4(p.C.at(z) + off, full4, cnt, in.c);
+  if constexpr (EPI != EPI_STORE && EPI != EPI_RESID) {
+    epi_ld4(p.X_in.at(z) + off, full4, cnt, in.x);
+    if constexpr (EPI == EPI_RK) {
+      if (p.stage > 1) epi_ld4(p.S.at(z) + off, full4, cnt, in.s);
+    }
+    if constexpr (EPI == EPI_ACCEL) {
+      if ((z & 1) == 0) epi_ld4(p.S.at(z) + off, full4, cnt, in.s);
+    }
+    if constexpr (EPI == EPI_EULER_CORR) {
+      epi_ld4(p.Gold.at(z) + off, full4, cnt, in.s);
+      epi_ld4(p.F_in.at(z) + off, full4, cnt, in.f);
+    }
+  }
+}
+
 // DEFER (symmetric mode only): the mirrored stores are not issued; the values of the (up to two)
 // output arrays land in mv[slot][0..3] and the arrays' base pointers in mp[slot] (null = unused),
 // so the caller can write the mirrors coalesced through a shared-memory transpose.
-template <int EPI, bool DEFER>
+template <int EPI, bool DEFER, bool PRE = false>
 __device__ __forceinline__ void epi_apply4_impl(const GemmParams& p, int z, double alpha, int row, int col, int n,
                                                 int ld, double (&k4)[4], bool sym, bool diag, double& part,
-                                                double (&mv)[2][4], double* (&mp)[2]) {
+                                                double (&mv)[2][4], double* (&mp)[2], const EpiIn* pre = nullptr) {
   const long long off = (long long)row * ld + col;
   const bool full4 = (col + 3 < n);
   const int cnt = full4 ? 4 : (n - col);
   // K = alpha*acc + beta*C
-  if (p.beta != 0.0) {
+  if (PRE && p.beta != 0.0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) k4[e] = fma(alpha, k4[e], p.beta * pre->c[e]);
+  } else if (p.beta != 0.0) {
     const double* Cp = p.C.at(z) + off;
     if (full4) {
       const double2 c0 = *reinterpret_cast<const double2*>(Cp);
@@ -58,7 +100,10 @@ __device__ __forceinline__ void epi_apply4_impl(const GemmParams& p, int z, doub
   } else {
     // load X (and S / Fk / Gold as needed)
     const double* Xp = p.X_in.at(z) + off;
-    if (full4) {
+    if (PRE) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) in0[e] = pre->x[e];
+    } else if (full4) {
       const double2 a0 = *reinterpret_cast<const double2*>(Xp);
       const double2 a1 = *reinterpret_cast<const double2*>(Xp + 2);
       in0[0] = a0.x; in0[1] = a0.y; in0[2] = a1.x; in0[3] = a1.y;
@@ -71,7 +116,10 @@ __device__ __forceinline__ void epi_apply4_impl(const GemmParams& p, int z, doub
     if constexpr (EPI == EPI_EULER_CORR) Sp = p.Gold.at(z) + off;
     if constexpr (EPI == EPI_RK || EPI == EPI_EULER_CORR || EPI == EPI_ACCEL) {
       if (EPI == EPI_EULER_CORR || (EPI == EPI_RK && p.stage > 1) || (EPI == EPI_ACCEL && (z & 1) == 0)) {
-        if (full4) {
+        if (PRE) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) in1[e] = pre->s[e];
+        } else if (full4) {
           const double2 a0 = *reinterpret_cast<const double2*>(Sp);
           const double2 a1 = *reinterpret_cast<const double2*>(Sp + 2);
           in1[0] = a0.x; in1[1] = a0.y; in1[2] = a1.x; in1[3] = a1.y;
@@ -111,7 +159,10 @@ __device__ __forceinline__ void epi_apply4_impl(const GemmParams& p, int z, doub
     } else if constexpr (EPI == EPI_EULER_CORR) {
       const double* Fp = p.F_in.at(z) + off;
       double fk[4];
-      if (full4) {
+      if (PRE) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) fk[e] = pre->f[e];
+      } else if (full4) {
         const double2 a0 = *reinterpret_cast<const double2*>(Fp);
         const double2 a1 = *reinterpret_cast<const double2*>(Fp + 2);
         fk[0] = a0.x; fk[1] = a0.y; fk[2] = a1.x; fk[3] = a1.y;

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   // the previous grid (all of its writes visible) before touching global memory.
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
+  if (cta_stop(p.stop_flag)) return;
 
   if constexpr (Cfg::kSetMaxNReg) {
     if (warp >= Cfg::kConsumerWarps)
@@ -354,6 +354,37 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         continue;
       }
     }
+    if constexpr (EPI != EPI_RESID) {
+      // epilogue over the flattened groups g = mt * NG + ng (guarded, no early exits).  EPI_STORE
+      // (W = B Y) runs the software-pipelined form (operands of group g + 1 loaded before group g is
+      // stored); the other epilogues keep their loads inline -- pipelining them raises register
+      // pressure past the 232-register budget of the 128 x 128 consumers without a measurable gain.
+      EpiIn buf[2];
+      if constexpr (EPI == EPI_STORE) {
+        const int row = m0 + wm * Cfg::WM + rowA, col = n0 + wn * Cfg::WN + 4 * c;
+        if (row < n && col < n) epi_load4<EPI>(p, z, row, col, n, ld, buf[0]);
+      }
+#pragma unroll
+      for (int gi = 0; gi < Cfg::MT * Cfg::NG; ++gi) {
+        const int mt = gi / Cfg::NG, ng = gi % Cfg::NG;
+        if constexpr (EPI == EPI_STORE) {
+          if (gi + 1 < Cfg::MT * Cfg::NG) {
+            const int mt1 = (gi + 1) / Cfg::NG, ng1 = (gi + 1) % Cfg::NG;
+            const int row1 = m0 + wm * Cfg::WM + mt1 * 8 + rowA, col1 = n0 + wn * Cfg::WN + ng1 * 16 + 4 * c;
+            if (row1 < n && col1 < n) epi_load4<EPI>(p, z, row1, col1, n, ld, buf[(gi + 1) & 1]);
+          }
+        }
+        const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
+        const int col = n0 + wn * Cfg::WN + ng * 16 + 4 * c;
+        if (row < n && col < n) {
+          double k4[4] = {acc[mt][2 * ng][0], acc[mt][2 * ng + 1][0], acc[mt][2 * ng][1], acc[mt][2 * ng + 1][1]};
+          double mv[2][4];
+          double* mp[2];
+          epi_apply4_impl<EPI, false, EPI == EPI_STORE>(p, z, alpha, row, col, n, ld, k4, false, false, part, mv, mp,
+                                                         &buf[gi & 1]);
+        }
+      }
+    } else {
 #pragma unroll
     for (int mt = 0; mt < Cfg::MT; ++mt) {
       const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
@@ -365,6 +396,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         double k4[4] = {acc[mt][2 * ng][0], acc[mt][2 * ng + 1][0], acc[mt][2 * ng][1], acc[mt][2 * ng + 1][1]};
         epi_apply4<EPI>(p, z, alpha, row, col, n, ld, k4, sym, m0 == n0, part);
       }
+    }
     }
     if constexpr (EPI == EPI_RESID) {
       // deterministic tile reduction: fixed shuffle tree, then warps in index order

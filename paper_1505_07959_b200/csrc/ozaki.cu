@@ -165,7 +165,7 @@ constexpr int kEncThreads = 128;
 __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab, long long mstride, int base, int step,
                                                               int n, int ld, uint8_t* planes, long long pstride,
                                                               int ldk, double* rscale, int nmod, int abits, const int* flag) {
-  if (flag != nullptr && *(volatile const int*)flag != 0) return;
+  if (cta_stop(flag)) return;
   const int row = blockIdx.x, z = blockIdx.y;
   const double* src = slab + (long long)(base + z * step) * mstride + (long long)row * ld;
   __shared__ double red[kEncThreads / 32];
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab,
 constexpr int kOzBad = 1 << 30;
 __global__ void k_oz_colexp(const double* slab, long long mstride, int base, int step, int n, int ld, int* colexp,
                             const int* flag) {
-  if (flag != nullptr && *(volatile const int*)flag != 0) return;
+  if (cta_stop(flag)) return;
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int z = blockIdx.z;
   const int r0 = blockIdx.y * 256;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) k_oz_enc_colsT(const double* slab, long l
                                                        int n, int ld, const int* colexp, uint8_t* planes,
                                                        long long pstride, int ldk, double* cscale, int nmod,
                                                        int abits, const int* flag) {
-  if (flag != nullptr && *(volatile const int*)flag != 0) return;
+  if (cta_stop(flag)) return;
   __shared__ double tile[kTT][kTT + 1];
   const int j0 = blockIdx.x * kTT, k0 = blockIdx.y * kTT, z = blockIdx.z;
   const double* src = slab + (long long)(base + z * step) * mstride;
@@ -461,7 +461,22 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  const bool stopped = (g.flag != nullptr && *(volatile const int*)g.flag != 0);   // same for both CTAs
+  // cancellation decided once per CTA and, for a CTA pair, OR-ed over both CTAs (the flag can flip
+  // between the two reads): a half-cancelled pair would wait forever on the other CTA's barriers
+  bool stopped = cta_stop(g.flag);
+  if (PAIR) {
+    __shared__ int s_pair_stop;
+    if (threadIdx.x == 0) s_pair_stop = stopped ? 1 : 0;
+    cluster_sync_all();
+    uint32_t peer_stop = 0;
+    asm volatile(
+        "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %1, %2;\n ld.shared::cluster.u32 %0, [ra];\n}\n"
+        : "=r"(peer_stop)
+        : "r"(smem_u32(&s_pair_stop)), "r"(rank ^ 1u)
+        : "memory");
+    stopped = stopped || peer_stop != 0;
+    cluster_sync_all();   // the peer's flag word is read before either CTA can exit
+  }
 
   if (!stopped && warp == 0 && lane == 0) {
     // ===================== TMA producer =====================
@@ -615,7 +630,7 @@ __global__ void __launch_bounds__(256, 4) k_oz_decode(const GemmParams p, const 
   // elements are stored directly and their mirrors are written through a shared-memory transpose
   // (32-byte row segments instead of scattered 8-byte column stores).
   const OzConst& c = c_oz[nmod];
-  if (p.stop_flag != nullptr && *(volatile const int*)p.stop_flag != 0) return;
+  if (cta_stop(p.stop_flag)) return;
   const int n = p.n;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   const int col = c0 + 4 * (threadIdx.x & 7);

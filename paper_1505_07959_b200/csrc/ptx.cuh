@@ -68,6 +68,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---- speculative-launch cancellation ----------------------------------------------------------
+// The stop flag is set by the metric kernel on another stream while a speculative launch may be
+// starting, so threads reading it individually could disagree (some warps returning, others then
+// waiting forever on barriers).  One thread reads it and the CTA agrees; must be called by every
+// thread of the CTA, outside divergent code.
+__device__ __forceinline__ bool cta_stop(const int* flag) {
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (flag != nullptr && *(volatile const int*)flag != 0) ? 1 : 0;
+  __syncthreads();
+  return s_stop != 0;
+}
+
 // ---- TMA ----------------------------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     fine_smem_kernel(int flow, int n, int ld, const double* __restrict__ M, const double* __restrict__ Uin,
                      double* __restrict__ Fout, long long mstride, int mF, double h, const int* stop_flag) {
   using C = SmallCfg<NP>;
-  if (stop_flag != nullptr && *(volatile const int*)stop_flag != 0) return;
+  if (cta_stop(stop_flag)) return;
   extern __shared__ double sm[];
   double* sM = sm;
   double* sX = sM + C::MAT;

@@ -482,3 +482,22 @@ def test_symmetric_mode_repeatable_inverse_n2048():
     for X in outs:
         assert np.array_equal(X, outs[0])
     assert relF(outs[0], ref) <= 1e-13
+
+
+@pytest.mark.timeout(600)
+def test_speculative_cancellation_never_hangs():
+    """Regression (round 1): a speculative launch reads the stop flag the metric kernel sets on the
+    coarse stream; when each thread read it on its own, a flip in mid-launch could cancel some warps
+    of a CTA (or one CTA of a pair) and leave the rest waiting on barriers forever (seen as cfg[2]
+    with K_max = 16 hanging after convergence at k = 8).  The decision is now CTA- (and pair-)
+    uniform.  Many converging tolerance-stopped solves with speculation, DMMA and emulated GEMMs."""
+    w = workloads.random_spd(1024, 9)
+    for emu in (0, 16):
+        s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, 16, 1, 3)
+        s.set_option("emulation", emu)
+        ks = set()
+        for _ in range(8):
+            info = s.solve(16, 1e-9, mf.STOP_DELTA)
+            ks.add(info["k_done"])
+        assert len(ks) == 1 and ks.pop() < 16
+        s.close()
