@@ -332,6 +332,9 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "traffic_algorithmic_bytes_per_launch": traffic.get("algorithmic_bytes_per_launch")
+                         if traffic else None,
+                         "traffic_note": traffic.get("note") if traffic else None,
                          "kernel": "dgemm_tma_kernel<128,128,2,4,4,EPI_RK> (fused RK4-stage FP64 DMMA GEMM)",
                          "launches": kla, "kernel_ms": kms,
                          "peak_source": "measured FP64 DMMA probe (profiles/fp64_peaks_r01.json); "
