@@ -167,7 +167,10 @@ MFODE_API int mfode_get_slice(mfode_ctx *h, int n_index, double *U);
  * shared-memory persistent kernels, default for n <= 64; 0 = one launch per GEMM), "symmetric" (1 = f3(i)
  * half-flop symmetric GEMMs, needs A == A^T bitwise), "emulation" (f3(ii): 0 = FP64 DMMA GEMMs;
  * 8..16 = every GEMM except the residual's emulated on the int8 tensor cores with that many CRT
- * moduli, see mfode_dgemm_emulated; EINVAL if n leaves fewer than 8 bits per operand). */
+ * moduli, see mfode_dgemm_emulated; EINVAL if n leaves fewer than 8 bits per operand).  Process-wide
+ * keys (they affect every handle of the process): "pdl" (1 = programmatic dependent launch of
+ * consecutive GEMMs, default; 0 = plain stream order), "oz_pair" (1 = CTA-pair int8 GEMM kernel,
+ * default; 0 = single-CTA kernel; results are bitwise identical). */
 MFODE_API int mfode_set_option(mfode_ctx *h, const char *key, int64_t value);
 
 MFODE_API const char *mfode_last_error(const mfode_ctx *h);
