@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab,
 #pragma unroll
   for (int w = 1; w < kEncThreads / 32; ++w) mx = fmax(mx, red[w]);
   const int e = (mx > 0.0) ? exp_of_max(mx) : 0;
-  const double scale = ldexp(1.0, abits - e);
+  // 2^(abits - e) as two factors so tiny rows (max < 2^-968) do not overflow the scale
+  const int sh1 = min(abits - e, 1000);
+  const double scale = ldexp(1.0, sh1), scale2 = ldexp(1.0, abits - e - sh1);
   if (threadIdx.x == 0) rscale[(long long)z * n + row] = bad_s ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, e - abits);
   uint8_t* dst = planes + (long long)z * nmod * pstride + (long long)row * ldk;
 #pragma unroll 2
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(kEncThreads) k_oz_enc_rows(const double* slab,
     }
     long long x[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) x[q] = bad_s ? 0LL : __double2ll_rn(v[q] * scale);
+    for (int q = 0; q < 4; ++q) x[q] = bad_s ? 0LL : __double2ll_rn(v[q] * scale * scale2);
     oz_write_residues4(dst + k, pstride, x, nmod);
   }
 }
@@ -268,10 +270,11 @@ __global__ void __launch_bounds__(256) k_oz_enc_colsT(const double* slab, long l
     const int ee = (e <= -kOzBad) ? 0 : e;
     if (blockIdx.y == 0 && kq == 0)
       cscale[(long long)z * n + j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, ee - abits);
-    const double scale = ldexp(1.0, abits - ee);
+    const int sh1 = min(abits - ee, 1000);
+    const double scale = ldexp(1.0, sh1), scale2 = ldexp(1.0, abits - ee - sh1);
     long long x[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) x[q] = bad ? 0LL : __double2ll_rn(tile[4 * kq + q][jj] * scale);
+    for (int q = 0; q < 4; ++q) x[q] = bad ? 0LL : __double2ll_rn(tile[4 * kq + q][jj] * scale * scale2);
     oz_write_residues4(dst + (long long)j * ldk + k, pstride, x, nmod);
   }
 }

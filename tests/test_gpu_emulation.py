@@ -312,3 +312,22 @@ def test_emulated_symmetric_inverse_reuses_encoding():
     assert relF(X1, ref["X"]) <= 1e-10
     _, _, X3 = _solve(A, mf.FLOW_INVERSE, T, N, mG, mF, K, 1e-11, mf.STOP_DELTA)
     assert relF(X1, X3) <= 1e-13
+
+
+def test_emulated_gemm_extreme_row_scales():
+    """Rows / columns of very different magnitude down to 1e-300: the power-of-two scaling never
+    overflows (the scale is applied as two factors) and each row of the product stays accurate
+    relative to its own scale."""
+    n = 96
+    rng = np.random.default_rng(21)
+    A = rng.standard_normal((n, n))
+    B = rng.standard_normal((n, n))
+    A[3] *= 1e-300
+    A[7] *= 1e250
+    B[:, 5] *= 1e-290
+    D = mf.dgemm_emulated(_dev(A), _dev(B)).cpu().numpy()
+    ref = A @ B
+    assert np.all(np.isfinite(D))
+    rowerr = np.abs(D - ref).max(1) / np.abs(ref).max(1)
+    assert rowerr.max() <= 1e-13
+    assert np.abs(D[:, 5] - ref[:, 5]).max() <= 1e-13 * np.abs(ref[:, 5]).max()
