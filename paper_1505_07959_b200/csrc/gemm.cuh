@@ -15,7 +15,7 @@
 //
 // FP64 on B200 has no tcgen05 kind (ptxas rejects kind::f64) and no wgmma, so the tensor path is
 // warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, measured 37.0 TF/s chip peak).  Structure:
-//   * persistent CTAs, static round-robin tile schedule over (z, tile_m, tile_n);
+//   * persistent CTAs, static round-robin tile schedule over (z, grouped tile raster);
 //   * one producer warp: one elected lane issues cp.async.bulk.tensor (TMA) loads of a
 //     BM x 16 A tile and BN/16 16x16 B boxes per k-step into a STAGES-deep mbarrier ring,
 //     128B swizzle (so fragment loads are bank-conflict free, see below);
@@ -102,11 +102,20 @@ struct GemmCfg {
 
 __device__ __forceinline__ int rho8(int g) { return ((g & 1) << 2) | (g >> 1); }
 
-// tile index r -> (tile_m, tile_n): row-major, or over the upper triangle tile_m <= tile_n (sym)
-__device__ __forceinline__ void tile_coords(bool sym, int r, int tiles_n, int& tm, int& tn) {
+// tile index r -> (tile_m, tile_n): grouped raster, or over the upper triangle tile_m <= tile_n (sym).
+// The grouped raster walks column-major inside bands of kGroupM tile rows, so the ~148 tiles in
+// flight cover about 8 x 18 tiles instead of 4.6 rows x all columns: at each k-step they share
+// fewer distinct A/B slabs, and fewer operand bytes are re-read from HBM once a batch exceeds L2.
+constexpr int kGroupM = 8;
+__device__ __forceinline__ void tile_coords(bool sym, int r, int tiles_m, int tiles_n, int& tm, int& tn) {
   if (!sym) {
-    tm = r / tiles_n;
-    tn = r - tm * tiles_n;
+    const int band = kGroupM * tiles_n;
+    const int b = r / band;
+    const int first = b * kGroupM;
+    const int rows = (tiles_m - first) < kGroupM ? (tiles_m - first) : kGroupM;
+    const int q = r - b * band;
+    tn = q / rows;
+    tm = first + (q - tn * rows);
     return;
   }
   tm = 0;
@@ -174,7 +183,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         const int z = t / tiles_per_z;
         const int r = t - z * tiles_per_z;
         int tm_, tn_;
-        tile_coords(sym, r, tiles_n, tm_, tn_);
+        tile_coords(sym, r, tiles_m, tiles_n, tm_, tn_);
         const int m0 = tm_ * BM;
         const int n0 = tn_ * BN;
         const int sa = p.a_base + z * p.a_step;
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     const int z = t / tiles_per_z;
     const int r = t - z * tiles_per_z;
     int tm_, tn_;
-    tile_coords(sym, r, tiles_n, tm_, tn_);
+    tile_coords(sym, r, tiles_m, tiles_n, tm_, tn_);
     const int m0 = tm_ * BM;
     const int n0 = tn_ * BN;
     const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
