@@ -9,6 +9,10 @@ Citations (P:n = PAPER.md line n):
   * steady-state flow dX/dt = F(X), F(X*) = 0 <=> X* = f(A)              P:46-51 eq. (stat)
     (instance F(X) = A - X^2, X* = A^{1/2}: BASELINE.json north star)
   * exponential flow dQ/dt = A Q, Q(0) = I, Q(1) = exp(A)                 Example 2
+  * affine (linear inhomogeneous) flow dU/dt = A U + G, U(0) = U0          eq. (eq1) P:72-76 with a
+    matrix state; Example 5's dX/dt = I - A X is the instance (A, G) -> (-A, I)
+  * modified parareal: Algorithm 3 (homogeneous), Algorithm 4 (inhomogeneous,
+    Step -1 and eq. (update2), P:404-432)
   * coarse propagator G = forward Euler                                   P:129, P:182 ("Euler explicit")
   * fine propagator F = Runge-Kutta ("Runge Kutta method can be applied") P:44; classical RK4 (R1)
   * Algorithm 1, Step 0 U^0_{n+1} = G(U^0_n), U^0_0 = u0                 P:136-139 eq. (eqStep0)
@@ -34,6 +38,7 @@ FLOW_INVERSE = 0
 FLOW_SQRT = 1
 FLOW_EXP = 2
 FLOW_TRIG = 3
+FLOW_AFFINE = 4
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
@@ -64,14 +69,21 @@ def rhs_trig(A: np.ndarray) -> Callable:
     return lambda U: np.vstack([A @ U[n:], -(A @ U[:n])])
 
 
+def rhs_affine(A: np.ndarray, Gsrc: np.ndarray) -> Callable:
+    """F(U) = A U + G: the linear inhomogeneous problem du/dt = A u + g of eq. (eq1) with
+    a matrix state (the "linear inhomogeneous case" of §3)."""
+    return lambda U: A @ U + Gsrc
+
+
 def initial_state(n: int, flow: int) -> np.ndarray:
-    """X0 = I; the trig block flow starts at (sin 0; cos 0) = (0; I)."""
+    """X0 = I; the trig block flow starts at (sin 0; cos 0) = (0; I).
+    The affine flow's default U0 is I as well (any U0 may be passed to the drivers)."""
     if flow == FLOW_TRIG:
         return np.vstack([np.zeros((n, n)), np.eye(n)])
     return np.eye(n)
 
 
-def make_rhs(A: np.ndarray, flow: int) -> Callable:
+def make_rhs(A: np.ndarray, flow: int, source: Optional[np.ndarray] = None) -> Callable:
     if flow == FLOW_INVERSE:
         B = np.eye(A.shape[0]) - A          # formed once (R2)
         return rhs_inverse(B)
@@ -81,6 +93,9 @@ def make_rhs(A: np.ndarray, flow: int) -> Callable:
         return rhs_exp(A)
     if flow == FLOW_TRIG:
         return rhs_trig(A)
+    if flow == FLOW_AFFINE:
+        n = A.shape[0]
+        return rhs_affine(A, np.zeros((n, n)) if source is None else np.asarray(source, dtype=np.float64))
     raise ValueError(f"unknown flow {flow}")
 
 
@@ -265,12 +280,76 @@ def modified_parareal(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K
     return out
 
 
+def modified_parareal_inhom(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K_max: int,
+                            tol: float = 0.0, stop: int = STOP_FIXED_K, rank_tol: float = 1e-12,
+                            keep_history: bool = False) -> dict:
+    """Algorithm 4: modified parareal for a linear INhomogeneous (affine) flow.
+      Step -1: F(T_{n+1}, T_n, 0) and G(T_{n+1}, T_n, 0) -- the flow is autonomous and the grid
+               uniform, so one F(0) and one G(0) serve every n (the same reading R18 as the fine
+               images of Algorithm 3).
+      Step 0:  identical to the homogeneous case, U^0_{n+1} = G(U^0_n), U^0_0 = U_0.
+      Step k+1: enhance S^k with U^k_0..U^k_N by globalQR (basis completed), F(Q_new) in parallel,
+               then eq. (update2):
+                 U^{k+1}_{n+1} = F(P_k U^{k+1}_n) + G((I - P_k) U^{k+1}_n) - G(0)
+               with the affine computation of the Remark:
+                 F(P_k U) = sum_i alpha_i {F(Q_i) - F(0)} + F(0),   P_k U = sum_i alpha_i Q_i.
+    With a zero source F(0) = G(0) = 0 exactly and this is Algorithm 3 bitwise (pinned)."""
+    hG = T / (N * m_G)
+    hF = T / (N * m_F)
+    G = lambda x: euler(rhs, x, hG, m_G)
+    F = lambda x: rk4(rhs, x, hF, m_F)
+    Z0 = np.zeros_like(X0)
+    F0 = F(Z0)                                               # Step -1
+    G0 = G(Z0)
+    U = [X0]                                                 # Step 0
+    for n in range(N):
+        U.append(G(U[n]))
+    Q, FQ = [], []
+    deltas = []
+    history = [list(U)] if keep_history else None
+    k_done = 0
+    converged = stop == STOP_FIXED_K
+    for k in range(min(K_max, N)):
+        nb_old = len(Q)
+        global_qr(U, Q, rank_tol)
+        for Qi in Q[nb_old:]:
+            FQ.append(F(Qi))
+        V = [X0]
+        for n in range(N):
+            alpha = [frob_inner(Qi, V[n]) for Qi in Q]
+            PV = sum(a * Qi for a, Qi in zip(alpha, Q))
+            FPV = sum(a * (Fi - F0) for a, Fi in zip(alpha, FQ)) + F0     # Remark, P:424-428
+            V.append(FPV + G(V[n] - PV) - G0)                              # eq. (update2)
+        delta = frob(V[N] - U[N]) / frob(V[N])
+        U = V
+        k_done = k + 1
+        deltas.append(delta)
+        if keep_history:
+            history.append(list(U))
+        if stop == STOP_DELTA and delta <= tol:
+            converged = True
+            break
+        if k_done == N:
+            converged = True
+            break
+    out = dict(X=U[N], U=U, k_done=k_done, deltas=deltas, converged=converged, basis=len(Q), F0=F0, G0=G0)
+    if keep_history:
+        out["history"] = history
+    return out
+
+
 def solve_modified(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,
-                   tol: float = 0.0, stop: int = STOP_FIXED_K, keep_history: bool = False) -> dict:
-    if flow not in (FLOW_EXP, FLOW_TRIG):
-        raise ValueError("Algorithm 3 is for linear homogeneous flows (exp, trig)")
+                   tol: float = 0.0, stop: int = STOP_FIXED_K, keep_history: bool = False,
+                   source: Optional[np.ndarray] = None, X0: Optional[np.ndarray] = None) -> dict:
+    """Algorithm 3 for the homogeneous flows (exp, trig); Algorithm 4 for the affine flow."""
     A = np.asarray(A, dtype=np.float64)
-    return modified_parareal(make_rhs(A, flow), initial_state(A.shape[0], flow), T, N, m_G, m_F, K_max, tol,
+    x0 = initial_state(A.shape[0], flow) if X0 is None else np.asarray(X0, dtype=np.float64)
+    if flow == FLOW_AFFINE:
+        return modified_parareal_inhom(make_rhs(A, flow, source), x0, T, N, m_G, m_F, K_max, tol, stop,
+                                       keep_history=keep_history)
+    if flow not in (FLOW_EXP, FLOW_TRIG):
+        raise ValueError("Algorithm 3 is for linear homogeneous flows (exp, trig); Algorithm 4 for affine")
+    return modified_parareal(make_rhs(A, flow), x0, T, N, m_G, m_F, K_max, tol,
                              stop, keep_history=keep_history)
 
 
@@ -307,19 +386,23 @@ def flow_residual(A: np.ndarray, flow: int) -> Optional[Callable]:
 
 def solve(A: np.ndarray, flow: int, T: float, N: int, m_G: int, m_F: int, K_max: int,
           tol: float = 0.0, stop: int = STOP_FIXED_K, skip_prefix: bool = True,
-          keep_history: bool = False) -> dict:
-    """f(A) by parareal on the flow's ODE with X0 = I."""
+          keep_history: bool = False, source: Optional[np.ndarray] = None,
+          X0: Optional[np.ndarray] = None) -> dict:
+    """f(A) by parareal on the flow's ODE with X0 = I; the affine flow takes a source G
+    and an optional U0."""
     A = np.asarray(A, dtype=np.float64)
-    rhs = make_rhs(A, flow)
-    X0 = initial_state(A.shape[0], flow)
+    rhs = make_rhs(A, flow, source)
+    X0 = initial_state(A.shape[0], flow) if X0 is None else np.asarray(X0, dtype=np.float64)
     # the residual is recorded for every flow; it drives the stop only for STOP_RESIDUAL
     return parareal(rhs, X0, T, N, m_G, m_F, K_max, tol, stop, frob, flow_residual(A, flow),
                     skip_prefix, keep_history)
 
 
-def solve_sequential_fine(A: np.ndarray, flow: int, T: float, N: int, m_F: int) -> np.ndarray:
+def solve_sequential_fine(A: np.ndarray, flow: int, T: float, N: int, m_F: int,
+                          source: Optional[np.ndarray] = None, X0: Optional[np.ndarray] = None) -> np.ndarray:
     A = np.asarray(A, dtype=np.float64)
-    return sequential_fine(make_rhs(A, flow), initial_state(A.shape[0], flow), T, N, m_F)[N]
+    x0 = initial_state(A.shape[0], flow) if X0 is None else np.asarray(X0, dtype=np.float64)
+    return sequential_fine(make_rhs(A, flow, source), x0, T, N, m_F)[N]
 
 
 def accel_inverse(A: np.ndarray, E0, dt: float, steps: int, X0=None):

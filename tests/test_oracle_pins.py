@@ -428,3 +428,136 @@ def test_config_workloads_shapes():
         lam = np.linalg.eigvalsh(w.A)
         assert np.allclose(np.sort(lam), np.sort(w.eigvals), rtol=1e-12, atol=1e-12)
     assert workloads.config(1).n == 256 and workloads.config(2).n == 1024
+
+
+# ---------------------------------------------------------------------------------------------
+# Affine (linear inhomogeneous) flow and Algorithm 4 (§3 "The linear inhomogeneous case")
+# ---------------------------------------------------------------------------------------------
+def _affine_closed_form(A, Gsrc, U0, t):
+    """u(t) = u0 + t phi(tA)(A u0 + g) (eq. eq1) for a MATRIX state, evaluated with the
+    library's expm of the augmented generator M = [[A, A U0 + G], [0, 0]]:
+    expm(tM) = [[e^{tA}, t phi(tA)(A U0 + G)], [0, I]]."""
+    import scipy.linalg
+    n = A.shape[0]
+    M = np.zeros((2 * n, 2 * n))
+    M[:n, :n] = A
+    M[:n, n:] = A @ U0 + Gsrc
+    return U0 + scipy.linalg.expm(t * M)[:n, n:]
+
+
+def test_affine_flow_closed_form_nonsymmetric():
+    """eq. (eq1) P:72-82 with a matrix state: the fine propagation of dU/dt = A U + G (A, G, U0
+    non-symmetric and non-commuting, so a transposed or dropped term fails) reaches the closed form
+    u0 + t phi(tA)(A u0 + g) within the RK4 truncation error; Euler within its first-order error."""
+    n = 7
+    A = workloads.random_nonsymmetric(n, 21, scale=1.0) - 1.5 * np.eye(n)
+    rng = np.random.default_rng(21)
+    Gs = rng.standard_normal((n, n))
+    U0 = rng.standard_normal((n, n))
+    ref = _affine_closed_form(A, Gs, U0, 1.0)
+    rhs = dense.make_rhs(A, dense.FLOW_AFFINE, Gs)
+    X = dense.rk4(rhs, U0, 1.0 / 64, 64)
+    assert dense.frob(X - ref) <= 1e-8 * dense.frob(ref)
+    Xe = dense.euler(rhs, U0, 1.0 / 4096, 4096)
+    err = dense.frob(Xe - ref) / dense.frob(ref)
+    assert 1e-6 < err < 1e-3
+    # Example 5 (P:680-686) is the instance (A, G) -> (-A, I), U0 = 0: X(t) -> A^{-1}
+    w = workloads.random_spd(n, 22, lo=1.0, hi=2.0)
+    Xs = dense.solve_sequential_fine(-w.A, dense.FLOW_AFFINE, 24.0, 8, 64, source=np.eye(n), X0=np.zeros((n, n)))
+    assert dense.frob(Xs - np.linalg.inv(w.A)) <= 1e-9 * dense.frob(np.linalg.inv(w.A))
+
+
+def test_affine_identity_of_the_fine_map():
+    """P:397-402: for a linear fine propagator F(a X + b Y) = a (F(X) - F(0)) + b (F(Y) - F(0)) + F(0);
+    the oracle's RK4 map on the affine flow satisfies it to rounding (an affine-ness bug, e.g. a
+    source term applied twice per stage, breaks it at O(h))."""
+    n = 6
+    A = workloads.random_nonsymmetric(n, 23, scale=1.0)
+    rng = np.random.default_rng(23)
+    Gs, X, Y = (rng.standard_normal((n, n)) for _ in range(3))
+    rhs = dense.make_rhs(A, dense.FLOW_AFFINE, Gs)
+    F = lambda Z: dense.rk4(rhs, Z, 1.0 / 40, 10)
+    a, b = 0.7, -1.9
+    lhs = F(a * X + b * Y)
+    F0 = F(np.zeros((n, n)))
+    rhs_ = a * (F(X) - F0) + b * (F(Y) - F0) + F0
+    assert dense.frob(lhs - rhs_) <= 1e-13 * dense.frob(lhs)
+    # the coarse map is affine too, and G(0) = m_G steps of Euler from 0 = h G + ... (one step: h G)
+    G1 = dense.euler(rhs, np.zeros((n, n)), 0.125, 1)
+    assert np.array_equal(G1, 0.125 * Gs)
+
+
+def test_algorithm4_zero_source_is_algorithm3_bitwise():
+    """With G = 0, Step -1 gives F(0) = G(0) = 0 exactly and eq. (update2) reduces to eq. (eq_update)
+    term by term: Algorithm 4 on the affine flow == Algorithm 3 on the exp flow, bitwise."""
+    n = 5
+    w = workloads.random_spd(n, 24, lo=0.5, hi=3.0)
+    N, mG, mF, K = 6, 1, 8, 3
+    m3 = dense.solve_modified(w.A, dense.FLOW_EXP, 1.0, N, mG, mF, K)
+    m4 = dense.solve_modified(w.A, dense.FLOW_AFFINE, 1.0, N, mG, mF, K, source=np.zeros((n, n)))
+    assert not np.any(m4["F0"]) and not np.any(m4["G0"])
+    assert m3["basis"] == m4["basis"] and m3["k_done"] == m4["k_done"]
+    for U3, U4 in zip(m3["U"], m4["U"]):
+        assert np.array_equal(U3, U4)
+
+
+def test_algorithm4_saturated_basis_is_fine_and_beats_classical():
+    """Algorithm 4: once S^k spans every iterate, P_k = I on them and eq. (update2) is
+    F(U) + G(0) - G(0) = F(U) -- the sequential fine solution (a dropped -G(0), or F(P U) without
+    the affine correction of the Remark P:424-428, breaks this).  n = 2: every iterate of every
+    propagator is r(A) W - C with W = U0 + A^{-1} G, C = A^{-1} G (Euler and RK4 share the fixed
+    point -A^{-1} G), so all of them lie in span{W, A W, C} (dimension 3), which the Step-0 iterates
+    already span: sweep 1 is the fine solution up to rounding -- far ahead of classical parareal;
+    the closed form eq1 confirms the fine solution itself."""
+    n = 2
+    A = workloads.random_nonsymmetric(n, 25, scale=1.0) - np.eye(n)
+    rng = np.random.default_rng(25)
+    Gs = rng.standard_normal((n, n))
+    U0 = rng.standard_normal((n, n))
+    N, mG, mF = 4, 1, 16
+    seq = dense.solve_sequential_fine(A, dense.FLOW_AFFINE, 1.0, N, mF, source=Gs, X0=U0)
+    m = dense.solve_modified(A, dense.FLOW_AFFINE, 1.0, N, mG, mF, 1, source=Gs, X0=U0)
+    assert m["basis"] == 3
+    assert dense.frob(m["X"] - seq) <= 1e-12 * dense.frob(seq)
+    c = dense.solve(A, dense.FLOW_AFFINE, 1.0, N, mG, mF, 1, source=Gs, X0=U0)
+    assert dense.frob(c["X"] - seq) > 1e3 * dense.frob(m["X"] - seq)
+    assert dense.frob(seq - _affine_closed_form(A, Gs, U0, 1.0)) <= 1e-7 * dense.frob(seq)
+    # larger n, commuting data: monotone dominance over classical parareal (P:489-490, S:223)
+    n = 10
+    w = workloads.random_spd(n, 26, lo=0.5, hi=2.0)
+    N, mG, mF = 8, 1, 8
+    src = np.eye(n)
+    seq = dense.solve_sequential_fine(-w.A, dense.FLOW_AFFINE, 4.0, N, mF, source=src, X0=np.zeros((n, n)))
+    for k in (1, 2, 3):
+        c = dense.solve(-w.A, dense.FLOW_AFFINE, 4.0, N, mG, mF, k, source=src, X0=np.zeros((n, n)))
+        m = dense.solve_modified(-w.A, dense.FLOW_AFFINE, 4.0, N, mG, mF, k, source=src, X0=np.zeros((n, n)))
+        assert dense.frob(m["X"] - seq) <= dense.frob(c["X"] - seq) * (1 + 1e-9) + 1e-14
+
+
+def test_affine_dense_vs_spectral():
+    """The spectral oracle's affine recursion x' = lam x + gamma (P1 with a commuting source) against
+    the dense oracle: Example 5's flow dX/dt = I - A X, X0 = 0, classical parareal."""
+    w = workloads.random_spd(12, 27, lo=0.5, hi=2.0)
+    N, mG, mF, K = 8, 2, 16, 4
+    d = dense.solve(-w.A, dense.FLOW_AFFINE, 3.0, N, mG, mF, K, source=np.eye(12), X0=np.zeros((12, 12)))
+    s = spectral.solve(-w.eigvals, dense.FLOW_AFFINE, 3.0, N, mG, mF, K, gamma=1.0, x0=0.0)
+    X = spectral.reconstruct(w.eigvecs, s["X"])
+    assert dense.frob(d["X"] - X) <= 1e-13 * dense.frob(X)
+    np.testing.assert_allclose(d["deltas"], s["deltas"], rtol=1e-9)
+
+
+def test_residual_definitions_closed_form():
+    """a8 residuals on hand-computed non-symmetric 2 x 2 cases where
+    ||A X - I|| != ||X A - I||: A = [[2, 1], [0, 1]], X = [[0, 0], [1, 0]] gives A X - I =
+    [[0, 0], [1, -1]] (Frobenius sqrt 2, so ||A X - I||_F / sqrt(n) = 1) while X A - I =
+    [[-1, 0], [2, 0]] (sqrt 5); a swapped product or a /n normalisation fails.  Square root:
+    A = [[4, 1], [0, 9]], X = [[2, 0.2], [0, 3]] has X^2 = A exactly (residual 0) while the
+    transposed square X X^T does not; X = 2 I gives A - X^2 = [[0, 1], [0, 5]], ||.||_F = sqrt 26,
+    ||A||_F = sqrt 98."""
+    A = np.array([[2.0, 1.0], [0.0, 1.0]])
+    X = np.array([[0.0, 0.0], [1.0, 0.0]])
+    assert dense.residual_inverse(A, X) == pytest.approx(1.0, rel=1e-15)
+    assert dense.residual_inverse(A, X) != pytest.approx(math.sqrt(5.0) / math.sqrt(2.0), rel=1e-3)
+    A = np.array([[4.0, 1.0], [0.0, 9.0]])
+    assert dense.residual_sqrt(A, np.array([[2.0, 0.2], [0.0, 3.0]])) == 0.0
+    assert dense.residual_sqrt(A, 2.0 * np.eye(2)) == pytest.approx(math.sqrt(26.0 / 98.0), rel=1e-15)
