@@ -106,8 +106,9 @@ class ClockSampler:
 
 def oracle_sample(w, budget_s=20.0):
     """The oracle as it stands on a bounded sample of the workload: fine RK4 steps of slice 0
-    (oracle.dense.rk4 with the flow's right-hand side), repeated until ~budget_s of CPU work.
-    Returns (tflops, seconds, steps, threads)."""
+    (oracle.dense.rk4 with the flow's right-hand side), repeated until ~budget_s/2 of CPU work.
+    Returns (tflops, seconds, steps, threads).  Runs in whatever process calls it; bench.py calls it
+    through cpu_baseline_subprocess() so that no CUDA context or torch thread pool competes."""
     import numpy as np
     from oracle import dense
     rhs = dense.make_rhs(w.A, w.flow)
@@ -131,6 +132,75 @@ def oracle_sample(w, budget_s=20.0):
     return flops_step * steps / dt / 1e12, dt, steps, threads or os.cpu_count()
 
 
+def host_description():
+    """nproc, the CPU model name and the BLAS / OpenMP thread settings of this host."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model,
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+_CPU_CHILD = r"""
+import json, os, sys
+sys.path.insert(0, sys.argv[1])
+import workloads
+import bench
+w = workloads.config(int(sys.argv[2]), with_eig=False)
+tf, dt, steps, threads = bench.oracle_sample(w, float(sys.argv[3]))
+info = {}
+try:
+    from threadpoolctl import threadpool_info
+    info = [{k: d.get(k) for k in ("internal_api", "num_threads", "version")} for d in threadpool_info()]
+except Exception:
+    pass
+print(json.dumps({"tflops": tf, "seconds": dt, "steps": steps, "threads": threads, "pools": info}))
+"""
+
+
+def cpu_baseline_subprocess(config, budget_s):
+    """Time the oracle sample in a fresh Python process (no torch, no CUDA context), so the repo arm's
+    cpu_baseline and the --impl reference arm measure the same program the same way."""
+    out = subprocess.run([sys.executable, "-c", _CPU_CHILD, ROOT, str(config), str(budget_s)],
+                         capture_output=True, text=True, timeout=600)
+    if out.returncode != 0:
+        raise RuntimeError(f"cpu baseline child failed: {out.stderr[-500:]}")
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    d.update(host_description())
+    return d
+
+
+def cpu_baseline_line(w, d):
+    return {"value": d["tflops"], "unit": UNIT, "cores": d["threads"], "kind": "oracle",
+            "sample": f"{d['steps']} RK4 step(s) of slice 0 of {w.name} with oracle.dense.rk4 "
+                      f"(numpy/OpenBLAS) in a fresh process, {d['seconds']:.1f} s",
+            "nproc": d["nproc"], "cpu_model": d["cpu_model"], "blas_pools": d.get("pools"),
+            "OMP_NUM_THREADS": d["OMP_NUM_THREADS"], "OPENBLAS_NUM_THREADS": d["OPENBLAS_NUM_THREADS"]}
+
+
+def spawn_ranks(args):
+    """--gpus N without a torchrun environment: re-launch this script as N ranks (one per GPU,
+    torch.distributed.run on 127.0.0.1).  Fails loudly when the box has fewer than N GPUs."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 3
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -144,11 +214,18 @@ def main():
     ap.add_argument("--emu-steps", type=int, default=1,
                     help="timed solves of the f3(ii) int8-tensor-core emulated variant (0: skip)")
     ap.add_argument("--emu-moduli", type=int, default=16)
+    ap.add_argument("--no-seqfine", action="store_true", help="skip timing mfode_sequential_fine (the K = N reference)")
     args = ap.parse_args()
 
+    in_torchrun = "WORLD_SIZE" in os.environ
+    if not in_torchrun and args.gpus > 1 and args.impl == "mine":
+        return spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "mine" and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 3
 
     import numpy as np
     import workloads
@@ -160,22 +237,31 @@ def main():
             return 0
         vals, secs = [], []
         for i in range(args.warmup + args.steps):
-            tf, dt, steps, threads = oracle_sample(w, budget_s=min(20.0, 120.0 / max(1, args.warmup + args.steps)))
+            d = cpu_baseline_subprocess(args.config, min(20.0, 120.0 / max(1, args.warmup + args.steps)))
             if i >= args.warmup:
-                vals.append(tf)
-                secs.append(dt)
+                vals.append(d["tflops"])
+                secs.append(d["seconds"])
         v = float(np.mean(vals))
-        sample = f"{steps} RK4 step(s) of slice 0 of {w.name} with oracle.dense.rk4 (numpy, OpenBLAS threads)"
+        cpu = cpu_baseline_line(w, d)
+        cpu["value"] = v
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "n": w.n, "N_slices": w.N, "m_G": w.m_G, "m_F": w.m_F,
                        "parallelism": "cpu"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
         return 0
+
+    # the CPU oracle sample first, in a fresh process, before this process creates a CUDA context
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_line(w, cpu_baseline_subprocess(args.config, 20.0))
+        except Exception as e:   # noqa: BLE001
+            cpu = {"error": str(e)}
 
     import torch
     import torch.distributed as dist
@@ -307,23 +393,51 @@ def main():
     emu_sym = (variant({"emulation": args.emu_moduli, "symmetric": 1}, args.emu_steps)
                if args.emu_steps > 0 else None)
 
+    # the K = N reference: sequential fine propagation through the same ranks (the
+    # same work as one GPU: each rank propagates its slices in turn and hands the state on)
+    seq = None
+    if not args.no_seqfine:
+        solver.set_option("phase_timing", 0)
+        barrier()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record()
+        sinfo = solver.sequential_fine()
+        q1.record()
+        q1.synchronize()
+        sq_ms = q0.elapsed_time(q1)
+        if world > 1:
+            t = torch.tensor([sq_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sq_ms = float(t.item())
+        solver.set_option("phase_timing", 1)
+        seq = {"ms": sq_ms, "fine_flops": sinfo["fine_flops"],
+               "tflops": sinfo["fine_flops"] / (sq_ms * 1e-3) / 1e12,
+               "speedup_parareal_vs_seqfine": sq_ms / ms_step,
+               "note": "T_seqfine / T_parareal(P): parareal does ~k_done x the fine work of the sequential "
+                       "reference, so this is bounded by ~P / k_done (SURVEY §8(d))"}
+
+    blocks = [list(mf.partition(w.N, world, r)) for r in range(world)]
+    phases = {k: float(np.mean([i[k] for i in infos])) for k in ("ms_coarse", "ms_correct", "ms_comm", "ms_metric",
+                                                                  "ms_fine", "ms_total")}
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            tf, dt, steps, threads = oracle_sample(w, budget_s=20.0)
-            cpu = {"value": tf, "unit": UNIT, "cores": threads, "kind": "oracle",
-                   "sample": f"{steps} RK4 step(s) of slice 0 of {w.name} with oracle.dense.rk4 "
-                             f"(numpy/OpenBLAS), {dt:.1f} s"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "host": host_description(),
             "config": {"workload": w.name, "n": w.n, "N_slices": w.N, "m_G": w.m_G, "m_F": w.m_F, "T": w.T,
                        "stop": "residual<=1e-10 (k>=1)" if w.stop == 2 else f"stop={w.stop} tol={w.tol}",
                        "global_batch": w.N, "parallelism": f"time-slices/{world} ranks",
                        "l2": "inputs larger than L2 (128 MiB per matrix, ~40 GiB working set); no flush"},
             "time_to_tol_ms": ms_step,
             "k_done": infos[-1]["k_done"],
+            "rank_slice_blocks": blocks,
+            "phases_ms_rank0_mean": phases,
+            "sequential_fine": seq,
+            "scaling_inputs": {"T_parareal_ms": ms_step, "n_gpus": world,
+                               "note": "E(P) = T_parareal(1) / (P T_parareal(P)) is computed by the driver from "
+                                       "the per-N lines; ms_comm is this rank's stream time in NCCL transfers"},
             "residual": resid,
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / max(1, args.e2e_steps),

@@ -66,15 +66,24 @@ typedef enum {
   MFODE_FLOW_INVERSE = 0, /* F(X) = X (I - A) X, X0 = I  => X(1) = A^{-1} */
   MFODE_FLOW_SQRT = 1,    /* F(X) = A - X^2,     X0 = I  => X(inf) = A^{1/2}         */
   MFODE_FLOW_EXP = 2,     /* F(X) = A X,         X0 = I  => X(1) = exp(A)       (Ex. 2) */
-  MFODE_FLOW_TRIG = 3     /* U = (X, Y), X' = A Y, Y' = -A X, U(0) = (0, I) => U(1) = (sin A, cos A)
+  MFODE_FLOW_TRIG = 3,    /* U = (X, Y), X' = A Y, Y' = -A X, U(0) = (0, I) => U(1) = (sin A, cos A)
                              (Ex. 3, eq. eqB P:441-456 with X0 = 0).  The state is the 2n x n stack
                              [X; Y]: results and slices are 2n x n (row-major, sin block first). */
+  MFODE_FLOW_AFFINE = 4   /* F(U) = A U + G, U(0) = U0: the linear inhomogeneous problem du/dt = Au + g
+                             of eq. (eq1) P:72-76 with a matrix state; G = 0 and U0 = I unless set by
+                             mfode_set_affine.  Example 5's dX/dt = I - A X (X -> A^{-1})
+                             is the instance (A, G) -> (-A, I).  Modified parareal: Algorithm 4. */
 } mfode_flow;
 
+/* Stop rules.  The paper gives none (it plots errors); DELTA is reading R6 (endpoint delta,
+ * BASELINE cfg[1]).  SPEC's CPU program uses max_n ||U^{k+1}_n - U^k_n||_F <= tol max(1,
+ * ||U_0||_F) instead: that is MFODE_STOP_MAX_SLICE.  All rules stop at k = N (R15). */
 typedef enum {
   MFODE_STOP_FIXED_K = 0,  /* exactly K_max correction sweeps (capped at N, reading R15)            */
   MFODE_STOP_DELTA = 1,    /* stop at the first k with ||U_N^k - U_N^{k-1}||_F/||U_N^k||_F <= tol  */
-  MFODE_STOP_RESIDUAL = 2  /* stop at the first k >= 1 with the flow residual <= tol (R10)         */
+  MFODE_STOP_RESIDUAL = 2, /* stop at the first k >= 1 with the flow residual <= tol (R10)         */
+  MFODE_STOP_MAX_SLICE = 3 /* stop at the first k with max_n ||U^k_n - U^{k-1}_n||_F
+                              <= tol * max(1, ||U_0||_F)  (SPEC classical_parareal)        */
 } mfode_stop;
 
 typedef struct {
@@ -101,7 +110,13 @@ typedef struct {
   double fine_kernel_ms;     /* summed CUDA-event duration of those launches (fine stream)       */
   double fine_kernel_flops;  /* flops those launches executed (algorithmic; in the symmetric
                                 mode only the upper-triangle tiles, i.e. ~half)                  */
-  double deltas[64];   /* delta of sweep k+1 in deltas[k] (first 64 sweeps)                     */
+  double deltas[64];   /* delta of sweep k+1 in deltas[k] (first 64 sweeps); MAX_SLICE: that metric */
+  int basis_size;      /* modified parareal: F-orthonormal basis blocks of S^k at return; else 0  */
+  /* Per-phase device time (CUDA events on the stream each phase runs on; summed over this
+   * process' ranks).  ms_coarse: Step 0; ms_correct: correction sweeps, coarse-stream busy time
+   * EXCLUDING the waits for fine results; ms_comm: boundary send/recv and metric broadcasts
+   * (stream time inside the transfers, including the wait for the peer); ms_metric: stop tests. */
+  double ms_coarse, ms_correct, ms_comm, ms_metric;
 } mfode_solve_info;
 
 /* ---- solver handle ------------------------------------------------------------------------ */
@@ -125,17 +140,26 @@ MFODE_API int mfode_create_device(mfode_ctx **out, const double *dA, int64_t n, 
  * caller solve for many matrices with one allocation.  Errors: EINVAL, ECUDA. */
 MFODE_API int mfode_set_matrix(mfode_ctx *h, const double *A);
 
+/* MFODE_FLOW_AFFINE only: set the source G (HOST row-major n*n, copied; NULL = 0) and the initial
+ * state U0 (HOST row-major n*n, copied; NULL = I) of dU/dt = A U + G (eq. eq1).  Collective
+ * in NCCL mode (rank 0 keeps U0).  Errors: EINVAL (other flows, NULL handle), ECUDA. */
+MFODE_API int mfode_set_affine(mfode_ctx *h, const double *G, const double *U0);
+
 /* Run Algorithm 1 from Step 0.  K_max >= 0 sweeps at most (0 = coarse sweep only); tol >= 0;
  * stop: mfode_stop.  Idempotent: each call restarts from Step 0.  info may be NULL.
  * Returns OK, NOT_CONVERGED (result valid), ENONFINITE, ECUDA, ENCCL, EINVAL. */
 MFODE_API int mfode_parareal_solve(mfode_ctx *h, int K_max, double tol, int stop, mfode_solve_info *info);
 
-/* Modified parareal for the linear homogeneous flows (MFODE_FLOW_EXP, MFODE_FLOW_TRIG):
+/* Modified parareal for the linear flows.  Homogeneous (MFODE_FLOW_EXP, MFODE_FLOW_TRIG):
  * Algorithm 3.  Each sweep enlarges S^k = span(S^{k-1} u {U^k_n}) with the global QR
- * of Algorithm 2 (modified Gram-Schmidt in the Frobenius inner product; blocks with
- * r_ii <= 1e-12 max(1, ||Z_i||_F) are eliminated), propagates only the NEW basis blocks with the
- * fine propagator (batched, one image per block since the flows are autonomous on a uniform
- * grid), then updates U^{k+1}_{n+1} = F(P U^{k+1}_n) + G((I - P) U^{k+1}_n) (eq. eq_update).
+ * of Algorithm 2 (Gram-Schmidt in the Frobenius inner product, applied twice -- reading
+ * R17; blocks with r_ii <= 1e-12 max(1, ||Z_i||_F) are eliminated, R16), propagates only the NEW
+ * basis blocks with the fine propagator (batched, one image per block since the flows are
+ * autonomous on a uniform grid), then updates U^{k+1}_{n+1} = F(P U^{k+1}_n) + G((I - P) U^{k+1}_n)
+ * (eq. eq_update).  Inhomogeneous (MFODE_FLOW_AFFINE): Algorithm 4 -- Step -1 computes
+ * F(0) and G(0) once, and eq. (update2) U^{k+1}_{n+1} = F(P U) + G((I - P) U) - G(0) uses
+ * F(P U) = sum_i alpha_i (F(Q_i) - F(0)) + F(0) (Remark P:424-428).  The Gram-Schmidt runs on the
+ * device (one host synchronisation per sweep); info->basis_size reports dim S^k.
  * max_basis (0 = (N+1)(min(K_max, N)+1)) caps the basis.  stop: FIXED_K or DELTA.  One rank.
  * Returns as mfode_parareal_solve; EINVAL for nonlinear flows or world > 1. */
 MFODE_API int mfode_modified_parareal_solve(mfode_ctx *h, int K_max, double tol, int stop, int max_basis,

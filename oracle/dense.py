@@ -24,7 +24,8 @@ Readings:
   R3 correction evaluated as F(U^k_n) + (G(U^{k+1}_n) - G(U^k_n))
   R4 U^{k+1}_0 = X0
   R5 K = number of correction sweeps after Step 0 (K = 0: coarse only)
-  R6 stop on delta_{k+1} = ||U^{k+1}_N - U^k_N||_F / ||U^{k+1}_N||_F <= tol (or fixed K)
+  R6 stop on delta_{k+1} = ||U^{k+1}_N - U^k_N||_F / ||U^{k+1}_N||_F <= tol (or fixed K); the SPEC
+     rule (S:194) max_n ||U^{k+1}_n - U^k_n||_F / max(1, ||U_0||_F) <= tol is STOP_MAX_SLICE
   R10 residual stop ||A - U_N^2||_F / ||A||_F <= tol evaluated only for k >= 1
 """
 from __future__ import annotations
@@ -42,6 +43,7 @@ FLOW_AFFINE = 4
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
+STOP_MAX_SLICE = 3   # SPEC classical_parareal: max_n ||U^{k+1}_n - U^k_n|| <= tol max(1, ||U_0||)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -173,7 +175,10 @@ def parareal(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K_max: int
             g = G(V[n])
             V[n + 1] = Fk[n] + (g - Gold[n])                  # R3
             Gold[n] = g
-        delta = norm(V[N] - U[N]) / norm(V[N])
+        if stop == STOP_MAX_SLICE:
+            delta = max(norm(V[n] - U[n]) for n in range(N + 1)) / max(1.0, norm(X0))
+        else:
+            delta = norm(V[N] - U[N]) / norm(V[N])
         U = V
         k_done = k + 1
         deltas.append(delta)
@@ -181,7 +186,7 @@ def parareal(rhs: Callable, X0, T: float, N: int, m_G: int, m_F: int, K_max: int
             residuals.append(residual(U[N]))
         if keep_history:
             history.append(list(U))
-        if stop == STOP_DELTA and delta <= tol:
+        if stop in (STOP_DELTA, STOP_MAX_SLICE) and delta <= tol:
             converged = True
             break
         if stop == STOP_RESIDUAL and residuals[-1] <= tol:      # k >= 1 by construction (R10)

@@ -24,9 +24,11 @@ FLOW_INVERSE = 0
 FLOW_SQRT = 1
 FLOW_EXP = 2
 FLOW_TRIG = 3      # state (sin, cos) stacked 2n x n (Example 3, eq. eqB)
+FLOW_AFFINE = 4    # dU/dt = A U + G, U(0) = U0 (eq. eq1; Example 5 with (A, G) -> (-A, I))
 STOP_FIXED_K = 0
 STOP_DELTA = 1
 STOP_RESIDUAL = 2
+STOP_MAX_SLICE = 3  # max_n ||U^{k+1}_n - U^k_n||_F <= tol max(1, ||U_0||_F)
 TILE_AUTO, TILE_128, TILE_64, TILE_32 = 0, 1, 2, 3
 
 OK, NOT_CONVERGED, EINVAL, ENOMEM, ECUDA, ENCCL, ENONFINITE = 0, 1, -1, -2, -3, -4, -5
@@ -37,14 +39,18 @@ EXPORTED = [
     "mfode_residual", "mfode_get_result", "mfode_get_result_device", "mfode_get_slice", "mfode_set_option",
     "mfode_last_error", "mfode_destroy", "mfode_dgemm", "mfode_rk_stage", "mfode_frobenius", "mfode_partition",
     "mfode_kernel_launches", "mfode_last_global_error", "mfode_version", "mfode_cosine", "mfode_accel_inverse",
-    "mfode_modified_parareal_solve", "mfode_dgemm_emulated", "mfode_release_workspace",
+    "mfode_modified_parareal_solve", "mfode_dgemm_emulated", "mfode_release_workspace", "mfode_set_affine",
 ]
 
 
 class MfodeError(RuntimeError):
-    def __init__(self, status: int, msg: str):
+    """A negative mfode_status.  ``info`` holds the solve's mfode_solve_info (as a dict) when the
+    failing call filled one -- e.g. ``info["bad_slice"]`` for MFODE_ENONFINITE."""
+
+    def __init__(self, status: int, msg: str, info: Optional[dict] = None):
         super().__init__(f"{_STATUS.get(status, status)}: {msg}")
         self.status = status
+        self.info = info
 
 
 class Dist(ctypes.Structure):
@@ -58,7 +64,9 @@ class SolveInfo(ctypes.Structure):
                 ("residual0", ctypes.c_double), ("ms_total", ctypes.c_double), ("ms_fine", ctypes.c_double),
                 ("fine_flops", ctypes.c_double), ("coarse_flops", ctypes.c_double), ("gpu_launches", ctypes.c_int),
                 ("fine_kernel_launches", ctypes.c_int), ("fine_kernel_ms", ctypes.c_double),
-                ("fine_kernel_flops", ctypes.c_double), ("deltas", ctypes.c_double * 64)]
+                ("fine_kernel_flops", ctypes.c_double), ("deltas", ctypes.c_double * 64),
+                ("basis_size", ctypes.c_int), ("ms_coarse", ctypes.c_double), ("ms_correct", ctypes.c_double),
+                ("ms_comm", ctypes.c_double), ("ms_metric", ctypes.c_double)]
 
     def to_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "deltas"}
@@ -83,6 +91,7 @@ def lib() -> ctypes.CDLL:
         "mfode_create": (I, [ctypes.POINTER(P), P, I64, I, D, I, I, I, ctypes.POINTER(Dist)]),
         "mfode_create_device": (I, [ctypes.POINTER(P), P, I64, I, D, I, I, I, ctypes.POINTER(Dist), P]),
         "mfode_set_matrix": (I, [P, P]),
+        "mfode_set_affine": (I, [P, P, P]),
         "mfode_parareal_solve": (I, [P, I, D, I, ctypes.POINTER(SolveInfo)]),
         "mfode_sequential_fine": (I, [P, ctypes.POINTER(SolveInfo)]),
         "mfode_residual": (I, [P, ctypes.POINTER(D)]),
@@ -114,11 +123,11 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-def _check(status: int, handle=None) -> int:
+def _check(status: int, handle=None, info: Optional["SolveInfo"] = None) -> int:
     if status < 0:
         L = lib()
         msg = L.mfode_last_error(handle) if handle else L.mfode_last_global_error()
-        raise MfodeError(status, (msg or b"").decode())
+        raise MfodeError(status, (msg or b"").decode(), info.to_dict() if info is not None else None)
     return status
 
 
@@ -198,21 +207,32 @@ class Solver:
         assert A.shape == (self.n, self.n)
         _check(lib().mfode_set_matrix(self._h, A.ctypes.data), self._h)
 
+    def set_affine(self, G: Optional[np.ndarray] = None, U0: Optional[np.ndarray] = None):
+        """FLOW_AFFINE: source G (None = 0) and initial state U0 (None = I) (mfode_set_affine)."""
+        def host(M):
+            if M is None:
+                return None
+            M = np.ascontiguousarray(M, dtype=np.float64)
+            assert M.shape == (self.n, self.n)
+            return M
+        G, U0 = host(G), host(U0)
+        _check(lib().mfode_set_affine(self._h, _ptr(G), _ptr(U0)), self._h)
+
     def set_option(self, key: str, value: int):
         _check(lib().mfode_set_option(self._h, key.encode(), int(value)), self._h)
 
     def solve(self, K_max: int, tol: float = 0.0, stop: int = STOP_FIXED_K) -> dict:
         info = SolveInfo()
-        st = _check(lib().mfode_parareal_solve(self._h, K_max, tol, stop, ctypes.byref(info)), self._h)
+        st = _check(lib().mfode_parareal_solve(self._h, K_max, tol, stop, ctypes.byref(info)), self._h, info)
         d = info.to_dict()
         d["status"] = _STATUS[st]
         return d
 
     def solve_modified(self, K_max: int, tol: float = 0.0, stop: int = STOP_FIXED_K, max_basis: int = 0) -> dict:
-        """Modified parareal, Algorithm 3 (linear homogeneous flows)."""
+        """Modified parareal: Algorithm 3 (exp, trig flows) or Algorithm 4 (affine flow)."""
         info = SolveInfo()
         st = _check(lib().mfode_modified_parareal_solve(self._h, K_max, tol, stop, max_basis, ctypes.byref(info)),
-                    self._h)
+                    self._h, info)
         d = info.to_dict()
         d["status"] = _STATUS[st]
         return d
@@ -246,13 +266,43 @@ class Solver:
 # ---------------------------------------------------------------------------------------------
 # kernel-level entry points (torch CUDA float64 tensors, row-major, leading dimension = stride(0))
 # ---------------------------------------------------------------------------------------------
+def _square_operands(named: dict, ref_name: str):
+    """Validate the device operands of a kernel-level call before raw pointers cross the ABI: every
+    tensor must be CUDA float64 on one device, n x n, unit column stride, with the SAME row stride
+    (the single leading dimension the C ABI takes) and 16-byte aligned.  Returns (n, ld)."""
+    ref = named[ref_name]
+    n = ref.shape[0]
+    ld = ref.stride(0)
+    for name, t in named.items():
+        if t is None:
+            continue
+        if not getattr(t, "is_cuda", False):
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if str(t.dtype) != "torch.float64":
+            raise ValueError(f"{name} must be float64, got {t.dtype}")
+        if t.device != ref.device:
+            raise ValueError(f"{name} is on {t.device}, {ref_name} on {ref.device}")
+        if t.dim() != 2 or tuple(t.shape) != (n, n):
+            raise ValueError(f"{name} must be {n} x {n}, got {tuple(t.shape)}")
+        if t.stride(1) != 1 or t.stride(0) != ld:
+            raise ValueError(f"{name} must be row-major with row stride {ld} (got strides {t.stride()}); "
+                             "transposed or differently padded views are not supported")
+        if t.data_ptr() % 16 != 0:
+            raise ValueError(f"{name} must be 16-byte aligned")
+    if ld < n or (ld * 8) % 16 != 0:
+        raise ValueError(f"row stride {ld} must be >= n = {n} and a multiple of 2 doubles")
+    return n, ld
+
 def dgemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, tile: int = TILE_AUTO, stream=None):
     """D = alpha A B + beta C on the B200 FP64 DMMA/TMA GEMM (mfode_dgemm)."""
     import torch
-    n = A.shape[0]
-    ld = A.stride(0)
     if out is None:
         out = torch.empty_strided(A.shape, A.stride(), dtype=A.dtype, device=A.device)
+    if beta != 0.0 and C is None:
+        raise ValueError("C is required when beta != 0")
+    n, ld = _square_operands({"A": A, "B": B, "C": C, "out": out}, "A")
+    if out.data_ptr() in (A.data_ptr(), B.data_ptr()):
+        raise ValueError("out must not alias A or B")
     _check(lib().mfode_dgemm(_ptr(A), _ptr(B), _ptr(C), _ptr(out), n, ld, alpha, beta, tile,
                              _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
     return out
@@ -262,10 +312,13 @@ def dgemm_emulated(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None
                    stream=None):
     """D = alpha A B + beta C emulated on the int8 tensor cores (mfode_dgemm_emulated, f3(ii))."""
     import torch
-    n = A.shape[0]
-    ld = A.stride(0)
     if out is None:
         out = torch.empty_strided(A.shape, A.stride(), dtype=A.dtype, device=A.device)
+    if beta != 0.0 and C is None:
+        raise ValueError("C is required when beta != 0")
+    n, ld = _square_operands({"A": A, "B": B, "C": C, "out": out}, "A")
+    if out.data_ptr() in (A.data_ptr(), B.data_ptr()):
+        raise ValueError("out must not alias A or B")
     _check(lib().mfode_dgemm_emulated(_ptr(A), _ptr(B), _ptr(C), _ptr(out), n, ld, alpha, beta, n_moduli,
                                       _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
     return out
@@ -281,7 +334,11 @@ def rk_stage(Yop, Bop, X, S, Ynext, stage: int, h: float, C=None, alpha: float =
              tile: int = TILE_AUTO, stream=None):
     """One fused RK4 stage (mfode_rk_stage): K = alpha Yop Bop + beta C, then the stage update."""
     import torch
-    n, ld = X.shape[0], X.stride(0)
+    if beta != 0.0 and C is None:
+        raise ValueError("C is required when beta != 0")
+    if stage < 4 and Ynext is None:
+        raise ValueError("Ynext is required for stages 1-3")
+    n, ld = _square_operands({"Yop": Yop, "Bop": Bop, "C": C, "X": X, "S": S, "Ynext": Ynext}, "X")
     _check(lib().mfode_rk_stage(_ptr(Yop), _ptr(Bop), _ptr(C), alpha, beta, _ptr(X), _ptr(S), _ptr(Ynext), stage,
                                 h, n, ld, tile,
                                 _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
@@ -291,7 +348,7 @@ def frobenius(X, Y=None, stream=None):
     """(||X - Y||_F, ||X||_F) by the library's deterministic reduction (mfode_frobenius)."""
     import torch
     out = (ctypes.c_double * 2)()
-    n, ld = X.shape[0], X.stride(0)
+    n, ld = _square_operands({"X": X, "Y": Y}, "X")
     _check(lib().mfode_frobenius(_ptr(X), _ptr(Y), n, ld, out,
                                  _stream_ptr(stream if stream is not None else torch.cuda.current_stream())))
     return out[0], out[1]

@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -50,6 +51,8 @@ static int set_global_err(int code, const char* fmt, ...) {
 struct NcclApi {
   bool ok = false;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+  ncclResult_t (*getVersion)(int*) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -71,6 +74,8 @@ static NcclApi& nccl() {
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) return api;
   api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+  api.commInitRankConfig = (decltype(api.commInitRankConfig))dlsym(h, "ncclCommInitRankConfig");
+  api.getVersion = (decltype(api.getVersion))dlsym(h, "ncclGetVersion");
   api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
   api.send = (decltype(api.send))dlsym(h, "ncclSend");
   api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
@@ -80,6 +85,15 @@ static NcclApi& nccl() {
   api.ok = api.commInitRank && api.commDestroy && api.send && api.recv && api.bcast && api.allreduce;
   return api;
 }
+
+// NVTX ranges around the host-side enqueue of each phase (visible to ncu --nvtx / nsys)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// per-phase device timing (mfode_solve_info ms_coarse / ms_correct / ms_comm / ms_metric)
+enum Phase : int { PH_COARSE = 0, PH_CORRECT = 1, PH_COMM = 2, PH_METRIC = 3, PH_COUNT = 4 };
 
 // ---------------------------------------------------------------------------------------------
 // context
@@ -98,7 +112,7 @@ struct Rank {
   std::vector<cudaEvent_t> evC;   // nloc: coarse-phase step j done
   std::vector<cudaEvent_t> evF;   // per fine chunk
   std::vector<int> chunk_of;      // nloc: fine chunk index of slice j (current sweep)
-  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_fine_end = nullptr, ev_metric = nullptr;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_fine_end = nullptr, ev_metric = nullptr, ev_aux = nullptr;
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;
   bool fine_started = false;
   // per-chunk timing of the fine GEMM launches (roofline of the dominant kernel)
@@ -109,6 +123,14 @@ struct Rank {
   };
   std::vector<ChunkTiming> tpool;
   int tused = 0;
+  // phase spans: pairs of timing events recorded on the stream the phase runs on
+  std::vector<cudaEvent_t> pev;
+  int pev_used = 0;
+  struct Span {
+    int phase, e0, e1;
+  };
+  std::vector<Span> spans;
+  double* spart = nullptr;   // per-slice partial sums (MAX_SLICE stop test)
 };
 
 }  // namespace mfode
@@ -133,6 +155,10 @@ struct mfode_ctx {
   bool overlap = true;
   int fine_batch_opt = 0;
   double normA = 0.0;        // ||A||_F
+  double normU0 = 0.0;       // ||U_0||_F (host; MAX_SLICE stop test)
+  double* Gsrc = nullptr;    // MFODE_FLOW_AFFINE: source G (device, zero by default)
+  double* X0dev = nullptr;   // MFODE_FLOW_AFFINE: U_0 (device copy; identity by default)
+  bool phase_timing = true;  // option "phase_timing"
   unsigned long long mat_gen = 0;   // content generation of A / B (emulated-GEMM encoding cache key)
   std::vector<mfode::Rank> ranks;
   // modified parareal (Algorithm 3): F-orthonormal basis Q of S^k, fine images F(Q), scratch
@@ -141,7 +167,13 @@ struct mfode_ctx {
   double* mtmp = nullptr;    // 3 states: P V, (I - P) V, G((I - P) V)
   double* coef = nullptr;    // device coefficients (bcap + 8)
   double* mpart = nullptr;   // multi-dot partials
-  int bcap = 0;
+  double* gstat = nullptr;   // device Gram-Schmidt statistics (4 per candidate block)
+  int* keep_dev = nullptr;   // device keep flags of the candidate blocks of a sweep
+  int* keep_host = nullptr;  // pinned copy
+  double* F0 = nullptr;      // Algorithm 4 Step -1: F(0), G(0) and a zero state
+  double* G0 = nullptr;
+  double* Z0 = nullptr;
+  int bcap = 0, kcap = 0;
   // result
   int result_rank = -1;
   const double* result_ptr = nullptr;
@@ -214,6 +246,53 @@ int partition(int N, int world, int rank, int* first, int* count) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// phase spans: a span is a pair of timing events on one stream; its duration counts towards one
+// phase of mfode_solve_info.  span_open returns -1 (and span_close does nothing) when disabled.
+// ---------------------------------------------------------------------------------------------
+static int span_event(mfode_ctx* h, Rank& R, cudaStream_t st, int* idx) {
+  if (R.pev_used == (int)R.pev.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(h, cudaEventCreate(&e));
+    R.pev.push_back(e);
+  }
+  *idx = R.pev_used++;
+  CUDA_TRY(h, cudaEventRecord(R.pev[*idx], st));
+  return MFODE_OK;
+}
+
+static int span_open(mfode_ctx* h, Rank& R, cudaStream_t st, int* open) {
+  *open = -1;
+  if (!h->phase_timing) return MFODE_OK;
+  return span_event(h, R, st, open);
+}
+
+static int span_close(mfode_ctx* h, Rank& R, cudaStream_t st, int phase, int* open) {
+  if (*open < 0) return MFODE_OK;
+  int e1;
+  TRY(span_event(h, R, st, &e1));
+  R.spans.push_back(Rank::Span{phase, *open, e1});
+  *open = -1;
+  return MFODE_OK;
+}
+
+// A span that is suspended around a cross-stream wait (the correction's wait for F(U^k_n)), so
+// that only the stream's busy time is counted.
+struct SpanCtx {
+  Rank* R;
+  cudaStream_t st;
+  int phase;
+  int open;
+};
+
+static int wait_in_span(mfode_ctx* h, SpanCtx* sc, cudaStream_t st, cudaEvent_t ev) {
+  const bool was_open = sc && sc->open >= 0;
+  if (was_open) TRY(span_close(h, *sc->R, sc->st, sc->phase, &sc->open));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, ev, 0));
+  if (was_open) TRY(span_open(h, *sc->R, sc->st, &sc->open));
+  return MFODE_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 // one GEMM-based step: K = F-operands ... with epilogue
 // ---------------------------------------------------------------------------------------------
 static GemmParams base_params(const mfode_ctx* h, int num_z) {
@@ -234,7 +313,7 @@ static GemmParams base_params(const mfode_ctx* h, int num_z) {
 // sqrt:    K = -(Y Y) + A with epilogue `epi`
 // exp:     K = A Y with epilogue `epi`
 static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, int num_z, GemmParams p, int epi,
-                      cudaStream_t st, cudaEvent_t wait_before_second) {
+                      cudaStream_t st, cudaEvent_t wait_before_second, SpanCtx* sc = nullptr) {
   const long long me = (long long)mat_elems(h);
   if (h->flow == MFODE_FLOW_INVERSE) {
     GemmParams q = base_params(h, num_z);
@@ -242,27 +321,32 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
     q.stop_flag = p.stop_flag;
     Operand Bop{h->B, 1, 0, 0, 0, h->mat_gen};
     CUDA_TRY(h, launch_gemm(EPI_STORE, h->tile, Bop, Y, q, st));
-    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    if (wait_before_second) TRY(wait_in_span(h, sc, st, wait_before_second));
     Operand Wop{Wbuf, Wcount, 0, 1};
     p.alpha = 1.0;
     p.beta = 0.0;
     p.oz_reuse_left = 1;   // Y was the right operand of the launch just above and is unchanged
     CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Wop, p, st));
   } else if (h->flow == MFODE_FLOW_SQRT) {
-    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    if (wait_before_second) TRY(wait_in_span(h, sc, st, wait_before_second));
     p.alpha = -1.0;
     p.beta = 1.0;
     p.C = MatRef{h->A, 0};
     CUDA_TRY(h, launch_gemm(epi, h->tile, Y, Y, p, st));
-  } else if (h->flow == MFODE_FLOW_EXP) {   // K = A Y
-    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+  } else if (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_AFFINE) {
+    // exp: K = A Y;  affine: K = A Y + G (eq. eq1, the source as the GEMM's beta term)
+    if (wait_before_second) TRY(wait_in_span(h, sc, st, wait_before_second));
     p.alpha = 1.0;
     p.beta = 0.0;
+    if (h->flow == MFODE_FLOW_AFFINE) {
+      p.beta = 1.0;
+      p.C = MatRef{h->Gsrc, 0};
+    }
     Operand Aop{h->A, 1, 0, 0, 0, h->mat_gen};
     CUDA_TRY(h, launch_gemm(epi, h->tile, Aop, Y, p, st));
   } else {   // MFODE_FLOW_TRIG: the batch runs over sub-matrices (X, Y) of each state:
              // K_X = A Y (even z), K_Y = -A X (odd z)  -- eq. (eqB) P:448-456 with X0 = 0
-    if (wait_before_second) CUDA_TRY(h, cudaStreamWaitEvent(st, wait_before_second, 0));
+    if (wait_before_second) TRY(wait_in_span(h, sc, st, wait_before_second));
     p.alpha = 1.0;
     p.beta = 0.0;
     p.alt_sign = 1;
@@ -279,7 +363,7 @@ static int flow_gemms(mfode_ctx* h, const Operand& Y, double* Wbuf, int Wcount, 
 //   EPI_EULER: Xout = g, and Gold (if non-null) = g
 //   EPI_EULER_CORR: Uout = Fk + (g - Gold); Gold = g  (waits `fk_ready` first)
 static int coarse_G(mfode_ctx* h, Rank& R, const double* in_slab, int in_count, int in_idx, int last_epi,
-                    double* Xout, double* Gold, double* Fk, cudaEvent_t fk_ready) {
+                    double* Xout, double* Gold, double* Fk, cudaEvent_t fk_ready, SpanCtx* sc = nullptr) {
   const double hG = h->T / ((double)h->N * h->mG);
   const long long me = (long long)mat_elems(h);
   const int ms = h->ms;
@@ -306,7 +390,8 @@ static int coarse_G(mfode_ctx* h, Rank& R, const double* in_slab, int in_count, 
       p.F_in = MatRef{Fk, me};
     }
     Operand Y{cur_slab, cur_count * ms, cur_idx * ms, 1};
-    TRY(flow_gemms(h, Y, R.Wc, 1, ms, p, epi, R.coarse, (last && last_epi == EPI_EULER_CORR) ? fk_ready : nullptr));
+    TRY(flow_gemms(h, Y, R.Wc, 1, ms, p, epi, R.coarse, (last && last_epi == EPI_EULER_CORR) ? fk_ready : nullptr,
+                   sc));
     cur_slab = tmp;
     cur_count = 1;
     cur_idx = 0;
@@ -399,6 +484,7 @@ static int fine_chunk_size(const mfode_ctx* h, int active) {
 
 static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
   if (k >= R.s1) return MFODE_OK;
+  NvtxRange nv(speculative ? "mfode:fine(speculative)" : "mfode:fine");
   const int ja0 = std::max(0, k - R.s0);
   const int active = R.nloc - ja0;
   if (active <= 0) return MFODE_OK;
@@ -447,7 +533,11 @@ static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
 static int send_boundary(mfode_ctx* h, Rank& R, int par) {
   if (R.id >= h->world - 1) return MFODE_OK;
   if (h->nccl_mode) {
+    NvtxRange nv("mfode:send_boundary");
+    int sp;
+    TRY(span_open(h, R, R.coarse, &sp));
     NCCL_TRY(h, nccl().send(slot(h, R.U[par], R.nloc), state_elems(h), ncclFloat64, R.id + 1, h->comm, R.coarse));
+    TRY(span_close(h, R, R.coarse, PH_COMM, &sp));
   } else {
     // logical ranks: the receiver copies after the sender's event (recorded in evC[nloc-1])
   }
@@ -456,44 +546,57 @@ static int send_boundary(mfode_ctx* h, Rank& R, int par) {
 
 static int recv_boundary(mfode_ctx* h, Rank& R, int par) {
   if (R.id == 0) return MFODE_OK;
+  NvtxRange nv("mfode:recv_boundary");
+  int sp;
   if (h->nccl_mode) {
+    TRY(span_open(h, R, R.coarse, &sp));
     NCCL_TRY(h, nccl().recv(R.U[par], state_elems(h), ncclFloat64, R.id - 1, h->comm, R.coarse));
   } else {
     Rank& P = h->ranks[R.id - 1];
     CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, P.evC[P.nloc - 1], 0));
+    TRY(span_open(h, R, R.coarse, &sp));
     CUDA_TRY(h, cudaMemcpyAsync(R.U[par], slot(h, P.U[par], P.nloc), state_elems(h) * sizeof(double),
                                 cudaMemcpyDeviceToDevice, R.coarse));
   }
+  TRY(span_close(h, R, R.coarse, PH_COMM, &sp));
   return MFODE_OK;
 }
 
 static int coarse_small_sweep(mfode_ctx* h, Rank& R, const double* Vin, double* Uslab, int j0, int correct) {
   const double hG = h->T / ((double)h->N * h->mG);
   const double* M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
+  int sp;
+  TRY(span_open(h, R, R.coarse, &sp));
   CUDA_TRY(h, launch_coarse_small(h->flow, h->n, h->ld, M, Vin, Uslab, R.Gold, R.Fk, (long long)mat_elems(h), j0,
                                   R.nloc, h->mG, hG, correct, R.coarse));
+  TRY(span_close(h, R, R.coarse, correct ? PH_CORRECT : PH_COARSE, &sp));
   for (int j = j0; j < R.nloc; ++j) CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
   return MFODE_OK;
 }
 
 static int enqueue_step0(mfode_ctx* h, Rank& R) {
+  NvtxRange nv("mfode:step0");
   TRY(recv_boundary(h, R, 0));
   if (h->small) {
     TRY(coarse_small_sweep(h, R, R.U[0], R.U[0], 0, 0));
     TRY(send_boundary(h, R, 0));
     return MFODE_OK;
   }
+  int sp;
+  TRY(span_open(h, R, R.coarse, &sp));
   for (int j = 0; j < R.nloc; ++j) {
     TRY(coarse_G(h, R, R.U[0], R.nloc + 1, j, EPI_EULER, slot(h, R.U[0], j + 1), slot(h, R.Gold, j), nullptr,
                  nullptr));
     CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
   }
+  TRY(span_close(h, R, R.coarse, PH_COARSE, &sp));
   TRY(send_boundary(h, R, 0));
   return MFODE_OK;
 }
 
 static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
   if (k >= R.s1) return MFODE_OK;
+  NvtxRange nv("mfode:correction");
   const int cur = k % 2, nxt = (k + 1) % 2;
   const int j0 = std::max(0, k - R.s0);
   if (k < R.s0) TRY(recv_boundary(h, R, nxt));
@@ -506,6 +609,8 @@ static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
     TRY(send_boundary(h, R, nxt));
     return MFODE_OK;
   }
+  SpanCtx sc{&R, R.coarse, PH_CORRECT, -1};
+  TRY(span_open(h, R, R.coarse, &sc.open));
   for (int j = j0; j < R.nloc; ++j) {
     const double* in_slab;
     int in_idx;
@@ -517,9 +622,10 @@ static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
       in_idx = j;
     }
     TRY(coarse_G(h, R, in_slab, R.nloc + 1, in_idx, EPI_EULER_CORR, slot(h, R.U[nxt], j + 1), slot(h, R.Gold, j),
-                 slot(h, R.Fk, j), R.evF[R.chunk_of[j]]));
+                 slot(h, R.Fk, j), R.evF[R.chunk_of[j]], &sc));
     CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
   }
+  TRY(span_close(h, R, R.coarse, PH_CORRECT, &sc.open));
   TRY(send_boundary(h, R, nxt));
   return MFODE_OK;
 }
@@ -566,6 +672,7 @@ static int alloc_rank(mfode_ctx* h, Rank& R) {
   const long long maxtiles = std::max<long long>(gemm_tiles(TILE_32, h->n, 1), kFrobPartials);
   CUDA_TRY(h, cudaMalloc(&R.partials, sizeof(double) * (maxtiles + 16)));
   CUDA_TRY(h, cudaMalloc(&R.metric, sizeof(double) * 8));
+  CUDA_TRY(h, cudaMalloc(&R.spart, sizeof(double) * 64 * (size_t)(R.nloc + 1)));
   CUDA_TRY(h, cudaMallocHost(&R.host_metric, sizeof(double) * 8));
   // zero everything once: padding columns stay zero forever (kernels never write them)
   CUDA_TRY(h, cudaMemset(R.U[0], 0, me * (R.nloc + 1)));
@@ -592,11 +699,12 @@ static int alloc_rank(mfode_ctx* h, Rank& R) {
   CUDA_TRY(h, cudaEventCreate(&R.ev_f1));
   CUDA_TRY(h, cudaEventCreateWithFlags(&R.ev_fine_end, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&R.ev_metric, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&R.ev_aux, cudaEventDisableTiming));
   return MFODE_OK;
 }
 
 static void free_rank(mfode_ctx* h, Rank& R) {
-  double* bufs[] = {R.U[0], R.U[1], R.Fk, R.Gold, R.Ya, R.Yb, R.W, R.S, R.Xa, R.Xb, R.Wc, R.partials, R.metric};
+  double* bufs[] = {R.U[0], R.U[1], R.Fk, R.Gold, R.Ya, R.Yb, R.W, R.S, R.Xa, R.Xb, R.Wc, R.partials, R.metric, R.spart};
   const size_t me = state_elems(h);
   for (double* b : bufs)
     if (b) {
@@ -620,7 +728,8 @@ static void free_rank(mfode_ctx* h, Rank& R) {
     cudaEventDestroy(ct.t0);
     cudaEventDestroy(ct.t1);
   }
-  cudaEvent_t evs[] = {R.ev_t0, R.ev_t1, R.ev_f0, R.ev_f1, R.ev_fine_end, R.ev_metric};
+  for (auto e : R.pev) cudaEventDestroy(e);
+  cudaEvent_t evs[] = {R.ev_t0, R.ev_t1, R.ev_f0, R.ev_f1, R.ev_fine_end, R.ev_metric, R.ev_aux};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
 }
@@ -669,7 +778,8 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   *out = nullptr;
   if (!A) return set_global_err(MFODE_EINVAL, "A is NULL");
   if (n < 1 || n > 65536) return set_global_err(MFODE_EINVAL, "n=%lld out of range [1, 65536]", (long long)n);
-  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT && flow != MFODE_FLOW_EXP && flow != MFODE_FLOW_TRIG)
+  if (flow != MFODE_FLOW_INVERSE && flow != MFODE_FLOW_SQRT && flow != MFODE_FLOW_EXP && flow != MFODE_FLOW_TRIG &&
+      flow != MFODE_FLOW_AFFINE)
     return set_global_err(MFODE_EINVAL, "unknown flow %d", flow);
   if (!(T > 0.0) || !std::isfinite(T)) return set_global_err(MFODE_EINVAL, "T must be finite and > 0");
   if (N < 1 || mG < 1 || mF < 1) return set_global_err(MFODE_EINVAL, "N, coarse_steps, fine_steps must be >= 1");
@@ -685,7 +795,9 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   h->mF = mF;
   h->world = world;
   h->ms = (flow == MFODE_FLOW_TRIG) ? 2 : 1;
-  h->small = (h->n <= kSmallMaxN) && h->ms == 1;
+  // K6 small-n kernels: the flows whose right-hand side they implement (not the affine source)
+  h->small = (h->n <= kSmallMaxN) && h->ms == 1 && flow != MFODE_FLOW_AFFINE;
+  h->normU0 = std::sqrt((double)n);   // ||I||_F (and ||(0; I)||_F for the trig flow)
   int dev = 0;
   if (dist) dev = dist->device;
   else cudaGetDevice(&dev);
@@ -698,7 +810,20 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
     if (!nccl().ok) return set_global_err(MFODE_ENCCL, "NCCL library not available (set MFODE_NCCL_LIB)");
     ncclUniqueId uid;
     memcpy(&uid, dist->nccl_uid, sizeof(uid));
-    ncclResult_t r = nccl().commInitRank(&h->comm, world, uid, dist->rank);
+    // Cap NCCL's CTAs (config.maxCTAs, default 8; env MFODE_NCCL_MAX_CTAS): a downstream rank posts
+    // its boundary receive while the upstream rank's fine sweep runs, and those NCCL kernels stay
+    // resident on SMs that the fine DMMA grid would otherwise use.
+    int ver = 0;
+    ncclResult_t r;
+    if (nccl().commInitRankConfig && nccl().getVersion && nccl().getVersion(&ver) == ncclSuccess && ver >= 22800) {
+      ncclConfig_t cfg = nccl_config_init(22809);
+      const char* mc = getenv("MFODE_NCCL_MAX_CTAS");
+      cfg.minCTAs = 1;
+      cfg.maxCTAs = mc ? std::max(1, atoi(mc)) : 8;
+      r = nccl().commInitRankConfig(&h->comm, world, uid, dist->rank, &cfg);
+    } else {
+      r = nccl().commInitRank(&h->comm, world, uid, dist->rank);
+    }
     if (r != ncclSuccess) return set_global_err(MFODE_ENCCL, "ncclCommInitRank failed: %d", (int)r);
   }
   // fine batch capacity: enough batched tiles to fill the chip, bounded by the slice count
@@ -729,6 +854,14 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
   if (flow == MFODE_FLOW_INVERSE) {
     if (cudaMalloc(&hp->B, me) != cudaSuccess) return set_global_err(MFODE_ENOMEM, "alloc B failed");
     cudaMemset(hp->B, 0, me);
+  }
+  if (flow == MFODE_FLOW_AFFINE) {   // source G = 0 and U_0 = I until mfode_set_affine
+    if (cudaMalloc(&hp->Gsrc, me) != cudaSuccess || cudaMalloc(&hp->X0dev, me) != cudaSuccess) {
+      mfode_destroy(h.release());
+      return set_global_err(MFODE_ENOMEM, "alloc source failed");
+    }
+    cudaMemset(hp->Gsrc, 0, me);
+    launch_identity(hp->X0dev, hp->n, hp->ld, 1, 0, nullptr);
   }
   if (cudaMalloc(&hp->stop_flag, sizeof(int)) != cudaSuccess) return set_global_err(MFODE_ENOMEM, "alloc flag failed");
   cudaMemset(hp->stop_flag, 0, sizeof(int));
@@ -777,7 +910,10 @@ static bool owns_last(mfode_ctx* h) { return last_rank(h).id == h->world - 1; }
 static int fetch_metric(mfode_ctx* h, int idx, int count) {
   Rank& L = last_rank(h);
   if (h->nccl_mode) {
+    int sp;
+    TRY(span_open(h, L, L.coarse, &sp));
     NCCL_TRY(h, nccl().bcast(L.metric + idx, L.metric + idx, count, ncclFloat64, h->world - 1, h->comm, L.coarse));
+    TRY(span_close(h, L, L.coarse, PH_COMM, &sp));
   }
   CUDA_TRY(h, cudaMemcpyAsync(L.host_metric + idx, L.metric + idx, count * sizeof(double), cudaMemcpyDeviceToHost,
                               L.coarse));
@@ -801,10 +937,63 @@ static int first_bad_slice(mfode_ctx* h) {
   return -1;
 }
 
+// Sum the recorded phase spans of every local rank into info (events already complete).
+static int collect_phases(mfode_ctx* h, mfode_solve_info* info) {
+  double ph[PH_COUNT] = {0.0, 0.0, 0.0, 0.0};
+  for (auto& R : h->ranks)
+    for (const auto& sp : R.spans) {
+      float ms = 0.f;
+      CUDA_TRY(h, cudaEventSynchronize(R.pev[sp.e1]));
+      CUDA_TRY(h, cudaEventElapsedTime(&ms, R.pev[sp.e0], R.pev[sp.e1]));
+      ph[sp.phase] += ms;
+    }
+  info->ms_coarse = ph[PH_COARSE];
+  info->ms_correct = ph[PH_CORRECT];
+  info->ms_comm = ph[PH_COMM];
+  info->ms_metric = ph[PH_METRIC];
+  return MFODE_OK;
+}
+
+// SPEC's stop metric: max_n ||U^{k+1}_n - U^k_n||_F / max(1, ||U_0||_F) over every slice of
+// every rank -> last rank's metric[0] (and `flag`).  Slices n <= k are unchanged by sweep k (R14).
+static int enqueue_max_slice(mfode_ctx* h, int k, double tol, int* flag) {
+  const int nxt = (k + 1) % 2, cur = k % 2;
+  const double denom = std::max(1.0, h->normU0);
+  Rank& L = last_rank(h);
+  std::vector<const double*> parts;
+  for (auto& R : h->ranks) {
+    const int jf = std::max(1, k + 1 - R.s0);   // local slot j <-> global slice s0 + j
+    const int count = (k < R.s1) ? std::max(0, R.nloc - jf + 1) : 0;
+    int sp;
+    TRY(span_open(h, R, R.coarse, &sp));
+    CUDA_TRY(h, launch_frob_slices_max(slot(h, R.U[nxt], jf), slot(h, R.U[cur], jf), (long long)state_elems(h), count,
+                                       (long long)state_elems(h), R.spart, R.metric + 3, R.coarse));
+    TRY(span_close(h, R, R.coarse, PH_METRIC, &sp));
+    if (h->nccl_mode) {
+      int sc;
+      TRY(span_open(h, R, R.coarse, &sc));
+      NCCL_TRY(h, nccl().allreduce(R.metric + 3, R.metric + 3, 1, ncclFloat64, ncclMax, h->comm, R.coarse));
+      TRY(span_close(h, R, R.coarse, PH_COMM, &sc));
+      const double* one = R.metric + 3;
+      CUDA_TRY(h, launch_max_ptrs(&one, 1, denom, R.metric + 0, tol, nullptr, R.coarse));
+    } else {
+      parts.push_back(R.metric + 3);
+      if (&R != &L) {
+        CUDA_TRY(h, cudaEventRecord(R.ev_aux, R.coarse));
+        CUDA_TRY(h, cudaStreamWaitEvent(L.coarse, R.ev_aux, 0));
+      }
+    }
+  }
+  if (!h->nccl_mode) CUDA_TRY(h, launch_max_ptrs(parts.data(), (int)parts.size(), denom, L.metric + 0, tol, flag, L.coarse));
+  return MFODE_OK;
+}
+
 static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
-  if (K_max < 0 || !(tol >= 0.0) || stop < 0 || stop > 2) return fail(h, MFODE_EINVAL, "bad K_max/tol/stop");
-  if (stop == MFODE_STOP_RESIDUAL && (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_TRIG))
-    return fail(h, MFODE_EINVAL, "the exp/trig flows have no residual stop test");
+  if (K_max < 0 || !(tol >= 0.0) || stop < 0 || stop > 3) return fail(h, MFODE_EINVAL, "bad K_max/tol/stop");
+  if (stop == MFODE_STOP_MAX_SLICE && h->world > 64) return fail(h, MFODE_EINVAL, "MAX_SLICE needs world <= 64");
+  if (stop == MFODE_STOP_RESIDUAL && (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_TRIG ||
+                                      h->flow == MFODE_FLOW_AFFINE))
+    return fail(h, MFODE_EINVAL, "the exp/trig/affine flows have no residual stop test");
   CUDA_TRY(h, cudaSetDevice(h->device));
   const long long L0 = g_launches.load();
   const int K_eff = std::min(K_max, h->N);
@@ -827,13 +1016,20 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
   for (auto& R : h->ranks) {
     R.fine_started = false;
     R.tused = 0;
+    R.pev_used = 0;
+    R.spans.clear();
     CUDA_TRY(h, cudaEventRecord(R.ev_t0, R.coarse));
     CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_t0, 0));
   }
   // ---- Step 0 ----
   for (auto& R : h->ranks) TRY(enqueue_step0(h, R));
   double res0 = NAN;
-  if (stop == MFODE_STOP_RESIDUAL && owns_last(h)) TRY(enqueue_residual(h, L, L.U[0], L.nloc + 1, L.nloc, 1, 0.0, nullptr));
+  if (stop == MFODE_STOP_RESIDUAL && owns_last(h)) {
+    int sp;
+    TRY(span_open(h, L, L.coarse, &sp));
+    TRY(enqueue_residual(h, L, L.U[0], L.nloc + 1, L.nloc, 1, 0.0, nullptr));
+    TRY(span_close(h, L, L.coarse, PH_METRIC, &sp));
+  }
   if (stop == MFODE_STOP_RESIDUAL) {
     TRY(fetch_metric(h, 1, 1));
     CUDA_TRY(h, cudaEventSynchronize(L.ev_metric));
@@ -851,20 +1047,28 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
     // stop metric on the last rank: delta of U_N (always), residual (STOP_RESIDUAL)
     const int nxt = (k + 1) % 2, cur = k % 2;
     int* flag = nullptr;
-    if (owns_last(h)) {
-      flag = (stop == MFODE_STOP_DELTA && spec && !h->nccl_mode) ? h->stop_flag : nullptr;
-      CUDA_TRY(h, launch_frob(slot(h, L.U[nxt], L.nloc), slot(h, L.U[cur], L.nloc), h->ms * h->n, h->ld, L.partials,
-                              L.metric + 0, 0, tol, flag, L.coarse));
-      if (stop == MFODE_STOP_RESIDUAL) {
-        int* rflag = (spec && !h->nccl_mode) ? h->stop_flag : nullptr;
-        TRY(enqueue_residual(h, L, L.U[nxt], L.nloc + 1, L.nloc, 1, tol, rflag));
+    {
+      NvtxRange nv("mfode:metric");
+      if (stop == MFODE_STOP_MAX_SLICE) {
+        TRY(enqueue_max_slice(h, k, tol, (spec && !h->nccl_mode) ? h->stop_flag : nullptr));
+      } else if (owns_last(h)) {
+        int sp;
+        TRY(span_open(h, L, L.coarse, &sp));
+        flag = (stop == MFODE_STOP_DELTA && spec && !h->nccl_mode) ? h->stop_flag : nullptr;
+        CUDA_TRY(h, launch_frob(slot(h, L.U[nxt], L.nloc), slot(h, L.U[cur], L.nloc), h->ms * h->n, h->ld,
+                                L.partials, L.metric + 0, 0, tol, flag, L.coarse));
+        if (stop == MFODE_STOP_RESIDUAL) {
+          int* rflag = (spec && !h->nccl_mode) ? h->stop_flag : nullptr;
+          TRY(enqueue_residual(h, L, L.U[nxt], L.nloc + 1, L.nloc, 1, tol, rflag));
+        }
+        TRY(span_close(h, L, L.coarse, PH_METRIC, &sp));
       }
+      TRY(fetch_metric(h, 0, 2));
     }
-    TRY(fetch_metric(h, 0, 2));
     if (spec && h->nccl_mode) {
       // every rank sets its own flag from the broadcast metric
       for (auto& R : h->ranks)
-        CUDA_TRY(h, launch_copy_flag(R.metric + (stop == MFODE_STOP_DELTA ? 0 : 1), tol, h->stop_flag, R.coarse));
+        CUDA_TRY(h, launch_copy_flag(R.metric + (stop == MFODE_STOP_RESIDUAL ? 1 : 0), tol, h->stop_flag, R.coarse));
     }
     const bool more = (k + 1 < K_eff);
     if (more && (spec || stop == MFODE_STOP_FIXED_K))
@@ -880,7 +1084,7 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
       status = MFODE_ENONFINITE;
       break;
     }
-    if (stop == MFODE_STOP_DELTA && delta <= tol) {
+    if ((stop == MFODE_STOP_DELTA || stop == MFODE_STOP_MAX_SLICE) && delta <= tol) {
       converged = true;
       break;
     }
@@ -925,6 +1129,7 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
   }
   loc.ms_total = ms_max;
   loc.k_done = k_done;
+  TRY(collect_phases(h, &loc));
   for (auto& R : h->ranks)
     for (int i = 0; i < R.tused; ++i) {
       const Rank::ChunkTiming& ct = R.tpool[i];
@@ -970,14 +1175,23 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
 }
 
 // ---------------------------------------------------------------------------------------------
-// Modified parareal for linear homogeneous flows (Algorithm 3)
-//   Step 0 as Algorithm 1.  Step k+1: S^k = span(S^{k-1} u {U^k_n}) with an F-orthonormal basis
-//   extended by the global QR of Algorithm 2 (modified Gram-Schmidt in <.,.>_F; a block
-//   with r_ii <= 1e-12 max(1, ||Z_i||_F) is eliminated -- reading R16); the fine images F(Q_i) of the
-//   NEW basis blocks only are propagated in parallel (batched); the update (eq. eq_update)
-//     U^{k+1}_{n+1} = sum_i alpha_i F(Q_i) + G(U^{k+1}_n - sum_i alpha_i Q_i),  alpha = Q^T <> U^{k+1}_n
-//   is sequential.  The flows are autonomous and the grid uniform, so F(T_{n+1}, T_n, .) is the same
-//   linear map for every n and one image per basis block suffices (SPEC design decision).
+// Modified parareal for linear flows: Algorithm 3 (homogeneous) and Algorithm 4
+// (inhomogeneous)
+//   Step -1 (Algorithm 4 only): F(0) and G(0) -- one of each, the flow being autonomous on a
+//   uniform grid (reading R18).  Step 0 as Algorithm 1.  Step k+1: S^k = span(S^{k-1} u {U^k_n})
+//   with an F-orthonormal basis extended by the global QR of Algorithm 2 (Frobenius inner product,
+//   P:250-304; Gram-Schmidt applied twice, reading R17; a block with r_ii <= 1e-12 max(1, ||Z_i||_F)
+//   is eliminated, R16); the fine images F(Q_i) of the NEW basis blocks only are propagated in
+//   parallel (batched); the update is sequential:
+//     Alg. 3, eq. (eq_update):  U^{k+1}_{n+1} = sum_i a_i F(Q_i) + G(U - sum_i a_i Q_i)
+//     Alg. 4, eq. (update2):    U^{k+1}_{n+1} = (sum_i a_i (F(Q_i) - F(0)) + F(0)) + G(U - P U) - G(0)
+//   with a = Q^T <> U^{k+1}_n.  One image per basis block serves every n (reading R18).
+// Device-side Gram-Schmidt: the N + 1 candidate blocks of a sweep are orthogonalised in turn, each
+// against every earlier slot with a batched multi-dot and one linear combination per pass
+// (classical Gram-Schmidt applied twice, CGS2 -- the same projection as Algorithm 2's modified
+// Gram-Schmidt in exact arithmetic; DESIGN reading R17), and the keep decision stays on the
+// device: an eliminated block is zeroed in place (later projections onto it add exact zeros).
+// The host reads the keep flags once per sweep and compacts the basis.
 // ---------------------------------------------------------------------------------------------
 static double host_frob(mfode_ctx* h, Rank& R, const double* X, const double* Y, cudaStream_t st, int* err) {
   if (launch_frob(X, Y, h->ms * h->n, h->ld, R.partials, R.metric + 6, 1, 0.0, nullptr, st) != cudaSuccess ||
@@ -989,42 +1203,71 @@ static double host_frob(mfode_ctx* h, Rank& R, const double* X, const double* Y,
   return Y ? R.host_metric[6] : R.host_metric[7];
 }
 
+static void free_modified(mfode_ctx* h) {
+  const size_t se = state_elems(h);
+  double* bufs[] = {h->Qb, h->FQ, h->mtmp};
+  for (double* b : bufs)
+    if (b) {
+      forget_maps(b, b + se * (size_t)(h->bcap + 3));
+      cudaFree(b);
+    }
+  double* small[] = {h->F0, h->G0, h->Z0};
+  for (double* b : small)
+    if (b) {
+      forget_maps(b, b + se);
+      cudaFree(b);
+    }
+  if (h->coef) cudaFree(h->coef);
+  if (h->mpart) cudaFree(h->mpart);
+  if (h->gstat) cudaFree(h->gstat);
+  if (h->keep_dev) cudaFree(h->keep_dev);
+  if (h->keep_host) cudaFreeHost(h->keep_host);
+  h->Qb = h->FQ = h->mtmp = h->coef = h->mpart = h->gstat = h->F0 = h->G0 = h->Z0 = nullptr;
+  h->keep_dev = h->keep_host = nullptr;
+  h->bcap = h->kcap = 0;
+}
+
 static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_basis, mfode_solve_info* info) {
   if (K_max < 0 || !(tol >= 0.0) || (stop != MFODE_STOP_FIXED_K && stop != MFODE_STOP_DELTA))
     return fail(h, MFODE_EINVAL, "bad K_max/tol/stop (modified parareal supports FIXED_K and DELTA)");
-  if (h->flow != MFODE_FLOW_EXP && h->flow != MFODE_FLOW_TRIG)
-    return fail(h, MFODE_EINVAL, "modified parareal (Algorithm 3) needs a linear homogeneous flow (exp, trig)");
+  if (h->flow != MFODE_FLOW_EXP && h->flow != MFODE_FLOW_TRIG && h->flow != MFODE_FLOW_AFFINE)
+    return fail(h, MFODE_EINVAL, "modified parareal needs a linear flow (exp, trig: Algorithm 3; affine: Algorithm 4)");
   if (h->world != 1) return fail(h, MFODE_EINVAL, "modified parareal runs on one rank");
   CUDA_TRY(h, cudaSetDevice(h->device));
   const long long L0 = g_launches.load();
   Rank& R = h->ranks[0];
   const int N = h->N;
+  const bool inhom = (h->flow == MFODE_FLOW_AFFINE);
   const size_t se = state_elems(h);
+  const long long tot = (long long)se;
   const int bcap = (max_basis > 0) ? max_basis : (N + 1) * (std::min(K_max, N) + 1);
-  if (bcap > h->bcap) {   // (re)allocate the basis storage
-    double* bufs[] = {h->Qb, h->FQ, h->mtmp};
-    for (double* b : bufs)
-      if (b) {
-        forget_maps(b, b + se * (size_t)(h->bcap + 3));
-        cudaFree(b);
-      }
-    if (h->coef) cudaFree(h->coef);
-    if (h->mpart) cudaFree(h->mpart);
-    h->Qb = h->FQ = h->mtmp = h->coef = h->mpart = nullptr;
-    h->bcap = 0;
+  if (bcap > h->bcap || N + 1 > h->kcap) {   // (re)allocate the basis storage
+    free_modified(h);
     CUDA_TRY(h, cudaMalloc(&h->Qb, se * bcap * sizeof(double)));
     CUDA_TRY(h, cudaMalloc(&h->FQ, se * bcap * sizeof(double)));
     CUDA_TRY(h, cudaMalloc(&h->mtmp, se * 3 * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->F0, se * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->G0, se * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->Z0, se * sizeof(double)));
     CUDA_TRY(h, cudaMalloc(&h->coef, (bcap + 8) * sizeof(double)));
     CUDA_TRY(h, cudaMalloc(&h->mpart, (size_t)std::min(bcap, 64) * 296 * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->gstat, (size_t)4 * (N + 1) * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&h->keep_dev, (size_t)(N + 1) * sizeof(int)));
+    CUDA_TRY(h, cudaMallocHost(&h->keep_host, (size_t)(N + 1) * sizeof(int)));
     CUDA_TRY(h, cudaMemset(h->Qb, 0, se * bcap * sizeof(double)));
     CUDA_TRY(h, cudaMemset(h->FQ, 0, se * bcap * sizeof(double)));
     CUDA_TRY(h, cudaMemset(h->mtmp, 0, se * 3 * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->F0, 0, se * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->G0, 0, se * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->Z0, 0, se * sizeof(double)));
     h->bcap = bcap;
+    h->kcap = N + 1;
   }
   cudaStream_t st = R.coarse;
   CUDA_TRY(h, cudaStreamSynchronize(R.fine));
   CUDA_TRY(h, cudaStreamSynchronize(st));
+  R.pev_used = 0;
+  R.spans.clear();
   mfode_solve_info loc;
   memset(&loc, 0, sizeof(loc));
   loc.bad_slice = -1;
@@ -1036,64 +1279,95 @@ static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_
   h->has_result = false;
   CUDA_TRY(h, cudaEventRecord(R.ev_t0, st));
   CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_t0, 0));
+  double fine_solves = 0.0;
+  if (inhom) {
+    // Step -1: F(0) on the fine stream, G(0) on the coarse stream
+    NvtxRange nv("mfode:step-1");
+    TRY(fine_prop(h, R, h->Z0, 1, h->F0, 1, 0, 1, nullptr));
+    TRY(coarse_G(h, R, h->Z0, 1, 0, EPI_EULER, h->G0, nullptr, nullptr, nullptr));
+    CUDA_TRY(h, cudaEventRecord(R.ev_fine_end, R.fine));
+    CUDA_TRY(h, cudaStreamWaitEvent(st, R.ev_fine_end, 0));
+    fine_solves += 1.0;
+  }
   TRY(enqueue_step0(h, R));   // U^0 in U[0]; slot 0 = X0 in both buffers
   int nb = 0, err = MFODE_OK, k_done = 0, status = MFODE_OK;
   bool converged = (stop == MFODE_STOP_FIXED_K);
-  double fine_solves = 0.0;
   double* Wv = h->mtmp + se;
   double* Gv = h->mtmp + 2 * se;
   const int K_eff = std::min(K_max, N);
   for (int k = 0; k < K_eff; ++k) {
     const int cur = k % 2, nxt = (k + 1) % 2;
-    // (a) enhance the subspace with U^k_0..U^k_N: Algorithm 2 (MGS in <.,.>_F), new blocks appended
+    // (a) enhance the subspace with U^k_0..U^k_N (Algorithm 2, device-side): candidate i goes to the
+    //     tentative slot nb + i; an eliminated candidate is zeroed there.
     const int nb_old = nb;
-    for (int n = 0; n <= N && nb < h->bcap; ++n) {
-      const double* Z = slot(h, R.U[cur], n);
-      double* q = slot(h, h->Qb, nb);
-      CUDA_TRY(h, cudaMemcpyAsync(q, Z, se * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      const double zn = host_frob(h, R, Z, nullptr, st, &err);
-      TRY(err);
-      for (int pass = 0; pass < 2; ++pass)   // two passes: reading R17 (reorthogonalisation)
-        for (int j = 0; j < nb; ++j) {       // r_ji = <Q, Q_j>_F; Q = Q - r_ji Q_j
-          CUDA_TRY(h, launch_multidot(slot(h, h->Qb, j), (long long)se, 1, q, (long long)se, h->mpart, h->coef, st));
-          CUDA_TRY(h, launch_axpy_dev(q, slot(h, h->Qb, j), h->coef, (long long)se, 0, st));
-        }
-      const double rii = host_frob(h, R, q, nullptr, st, &err);
-      TRY(err);
-      if (!std::isfinite(rii)) {
-        status = MFODE_ENONFINITE;
-        loc.bad_slice = n;
-        break;
+    const int ncand = std::min(N + 1, h->bcap - nb);
+    {
+      NvtxRange nv("mfode:global_qr");
+      for (int i = 0; i < ncand; ++i) {
+        const double* Z = slot(h, R.U[cur], i);
+        double* q = slot(h, h->Qb, nb + i);
+        double* gs = h->gstat + 4 * i;
+        CUDA_TRY(h, cudaMemcpyAsync(q, Z, se * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, launch_frob(Z, nullptr, h->ms * h->n, h->ld, R.partials, gs, 1, 0.0, nullptr, st));   // ||Z_i||
+        const int cnt = nb + i;
+        if (cnt > 0)
+          for (int pass = 0; pass < 2; ++pass) {   // reading R17: the projection applied twice
+            CUDA_TRY(h, launch_multidot(h->Qb, tot, cnt, q, tot, h->mpart, h->coef, st));    // r_j = <q, Q_j>_F
+            CUDA_TRY(h, launch_lincomb(q, h->Qb, tot, h->coef, cnt, tot, q, -1.0, st));       // q -= sum r_j Q_j
+          }
+        CUDA_TRY(h, launch_frob(q, nullptr, h->ms * h->n, h->ld, R.partials, gs + 2, 1, 0.0, nullptr, st));  // r_ii
+        CUDA_TRY(h, launch_gs_keep(q, tot, gs, 1e-12, h->keep_dev + i, st));
       }
-      if (rii > 1e-12 * std::max(1.0, zn)) {   // keep: Q_i = Q / r_ii
-        CUDA_TRY(h, cudaMemcpyAsync(h->coef, &R.host_metric[7], sizeof(double), cudaMemcpyHostToDevice, st));
-        CUDA_TRY(h, launch_axpy_dev(q, nullptr, h->coef, (long long)se, 1, st));
+      CUDA_TRY(h, cudaMemcpyAsync(h->keep_host, h->keep_dev, ncand * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(h, cudaStreamSynchronize(st));
+      for (int i = 0; i < ncand; ++i)
+        if (h->keep_host[i] == -1) {   // a non-finite iterate
+          status = MFODE_ENONFINITE;
+          loc.bad_slice = i;
+          break;
+        }
+      if (status < 0) break;
+      // compact the kept blocks (ascending; destination never after its source)
+      for (int i = 0; i < ncand; ++i) {
+        if (!h->keep_host[i]) continue;
+        if (nb != nb_old + i)
+          CUDA_TRY(h, cudaMemcpyAsync(slot(h, h->Qb, nb), slot(h, h->Qb, nb_old + i), se * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, st));
         ++nb;
       }
     }
-    if (status < 0) break;
     // (b) fine images of the new blocks, in parallel (batched over the blocks, chunks of `cap`)
     if (nb > nb_old) {
+      NvtxRange nv("mfode:fine_images");
       CUDA_TRY(h, cudaEventRecord(R.ev_metric, st));
       CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_metric, 0));
       for (int ja = nb_old; ja < nb; ja += h->cap) {
         const int jb = std::min(nb, ja + h->cap);
         TRY(fine_prop(h, R, h->Qb, h->bcap, h->FQ, h->bcap, ja, jb, nullptr));
       }
+      // Algorithm 4: keep D_i = F(Q_i) - F(0) (Remark P:424-428)
+      if (inhom) CUDA_TRY(h, launch_sub_bcast(slot(h, h->FQ, nb_old), tot, nb - nb_old, h->F0, tot, R.fine));
       fine_solves += nb - nb_old;
       CUDA_TRY(h, cudaEventRecord(R.ev_fine_end, R.fine));
       CUDA_TRY(h, cudaStreamWaitEvent(st, R.ev_fine_end, 0));
     }
-    // (c) sequential update (eq. eq_update): V_0 = X0
-    const double hG = h->T / ((double)N * h->mG);
-    (void)hG;
-    for (int n = 0; n < N; ++n) {
-      const double* V = slot(h, R.U[nxt], n);
-      CUDA_TRY(h, launch_multidot(h->Qb, (long long)se, nb, V, (long long)se, h->mpart, h->coef, st));
-      CUDA_TRY(h, launch_lincomb(Wv, h->Qb, (long long)se, h->coef, nb, (long long)se, V, -1.0, st));  // (I-P)V
-      TRY(coarse_G(h, R, Wv, 1, 0, EPI_EULER, Gv, nullptr, nullptr, nullptr));                        // G((I-P)V)
-      CUDA_TRY(h, launch_lincomb(slot(h, R.U[nxt], n + 1), h->FQ, (long long)se, h->coef, nb, (long long)se, Gv,
-                                 1.0, st));                                                            // + F(PV)
+    // (c) sequential update, V_0 = X0
+    {
+      NvtxRange nv("mfode:update");
+      SpanCtx sc{&R, st, PH_CORRECT, -1};
+      TRY(span_open(h, R, st, &sc.open));
+      for (int n = 0; n < N; ++n) {
+        const double* V = slot(h, R.U[nxt], n);
+        CUDA_TRY(h, launch_multidot(h->Qb, tot, nb, V, tot, h->mpart, h->coef, st));               // a = Q^T <> V
+        CUDA_TRY(h, launch_lincomb(Wv, h->Qb, tot, h->coef, nb, tot, V, -1.0, st));                 // (I - P) V
+        TRY(coarse_G(h, R, Wv, 1, 0, EPI_EULER, Gv, nullptr, nullptr, nullptr));                   // G((I - P) V)
+        if (inhom)
+          CUDA_TRY(h, launch_lincomb_affine(slot(h, R.U[nxt], n + 1), h->FQ, tot, h->coef, nb, tot, h->F0, Gv, h->G0,
+                                            st));                                                   // eq. (update2)
+        else
+          CUDA_TRY(h, launch_lincomb(slot(h, R.U[nxt], n + 1), h->FQ, tot, h->coef, nb, tot, Gv, 1.0, st));  // eq_update
+      }
+      TRY(span_close(h, R, st, PH_CORRECT, &sc.open));
     }
     const double num = host_frob(h, R, slot(h, R.U[nxt], N), slot(h, R.U[cur], N), st, &err);
     TRY(err);
@@ -1105,6 +1379,14 @@ static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_
     if (k < 64) loc.deltas[k] = delta;
     if (!std::isfinite(delta)) {
       status = MFODE_ENONFINITE;
+      for (int n = 0; n <= N; ++n) {   // first non-finite slice of the new iterate
+        const double v = host_frob(h, R, slot(h, R.U[nxt], n), nullptr, st, &err);
+        TRY(err);
+        if (!std::isfinite(v)) {
+          loc.bad_slice = n;
+          break;
+        }
+      }
       break;
     }
     if (stop == MFODE_STOP_DELTA && delta <= tol) {
@@ -1124,14 +1406,16 @@ static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_
   loc.ms_total = ms;
   loc.k_done = k_done;
   loc.converged = converged ? 1 : 0;
+  loc.basis_size = nb;
   loc.fine_flops = fine_solves * h->mF * rk4_flops(h);
   loc.coarse_flops = (double)N * (k_done + 1) * h->mG * euler_flops(h);
   loc.gpu_launches = (int)(g_launches.load() - L0);
+  TRY(collect_phases(h, &loc));
   h->result_rank = 0;
   h->result_ptr = slot(h, R.U[k_done % 2], R.nloc);
   h->has_result = true;
   if (info) *info = loc;
-  if (status < 0) return fail(h, status, "non-finite state in the modified parareal");
+  if (status < 0) return fail(h, status, "non-finite state in the modified parareal (first bad slice %d)", loc.bad_slice);
   if (!converged) {
     h->err = "not converged within K_max sweeps";
     return MFODE_NOT_CONVERGED;
@@ -1141,10 +1425,13 @@ static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_
 
 static int sequential_impl(mfode_ctx* h, mfode_solve_info* info) {
   CUDA_TRY(h, cudaSetDevice(h->device));
+  NvtxRange nv("mfode:sequential_fine");
   const long long L0 = g_launches.load();
   for (auto& R : h->ranks) {
     CUDA_TRY(h, cudaStreamSynchronize(R.fine));
     CUDA_TRY(h, cudaStreamSynchronize(R.coarse));
+    R.pev_used = 0;
+    R.spans.clear();
     CUDA_TRY(h, cudaEventRecord(R.ev_t0, R.coarse));
   }
   const int saved_cap = h->cap;
@@ -1228,6 +1515,40 @@ int mfode_set_matrix(mfode_ctx* h, const double* A) {
   return load_matrix(h, A, true, (size_t)h->n, h->ranks[0].coarse);
 }
 
+int mfode_set_affine(mfode_ctx* h, const double* G, const double* U0) {
+  if (!h) return set_global_err(MFODE_EINVAL, "NULL handle");
+  if (h->flow != MFODE_FLOW_AFFINE) return fail(h, MFODE_EINVAL, "mfode_set_affine needs MFODE_FLOW_AFFINE");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  for (auto& R : h->ranks) {
+    CUDA_TRY(h, cudaStreamSynchronize(R.fine));
+    CUDA_TRY(h, cudaStreamSynchronize(R.coarse));
+  }
+  cudaStream_t st = h->ranks[0].coarse;
+  const size_t rowb = (size_t)h->n * sizeof(double), ldb = (size_t)h->ld * sizeof(double);
+  oz_forget(h->Gsrc);
+  if (G)
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->Gsrc, ldb, G, rowb, rowb, h->n, cudaMemcpyHostToDevice, st));
+  else
+    CUDA_TRY(h, cudaMemsetAsync(h->Gsrc, 0, mat_elems(h) * sizeof(double), st));
+  if (U0) {
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->X0dev, ldb, U0, rowb, rowb, h->n, cudaMemcpyHostToDevice, st));
+    double ss = 0.0;
+    for (size_t i = 0; i < (size_t)h->n * h->n; ++i) ss += U0[i] * U0[i];
+    h->normU0 = std::sqrt(ss);
+  } else {
+    CUDA_TRY(h, launch_identity(h->X0dev, h->n, h->ld, 1, 0, st));
+    h->normU0 = std::sqrt((double)h->n);
+  }
+  // U_0 lives in slot 0 of both U buffers of rank 0
+  for (auto& R : h->ranks)
+    if (R.id == 0)
+      for (int b = 0; b < 2; ++b)
+        CUDA_TRY(h, cudaMemcpyAsync(R.U[b], h->X0dev, mat_elems(h) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  h->has_result = false;
+  return MFODE_OK;
+}
+
 int mfode_parareal_solve(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve_info* info) {
   if (!h) return set_global_err(MFODE_EINVAL, "NULL handle");
   return solve_impl(h, K_max, tol, stop, info);
@@ -1247,8 +1568,8 @@ int mfode_sequential_fine(mfode_ctx* h, mfode_solve_info* info) {
 int mfode_residual(mfode_ctx* h, double* rel) {
   if (!h || !rel) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!h->has_result) return fail(h, MFODE_EINVAL, "no result yet (call a solve first)");
-  if (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_TRIG)
-    return fail(h, MFODE_EINVAL, "the exp/trig flows have no residual");
+  if (h->flow == MFODE_FLOW_EXP || h->flow == MFODE_FLOW_TRIG || h->flow == MFODE_FLOW_AFFINE)
+    return fail(h, MFODE_EINVAL, "the exp/trig/affine flows have no residual");
   CUDA_TRY(h, cudaSetDevice(h->device));
   Rank& L = last_rank(h);
   if (owns_last(h)) {
@@ -1320,8 +1641,14 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     h->overlap = value != 0;
     return MFODE_OK;
   }
+  if (!strcmp(key, "phase_timing")) {   // per-phase CUDA-event spans (mfode_solve_info ms_coarse ...)
+    h->phase_timing = value != 0;
+    return MFODE_OK;
+  }
   if (!strcmp(key, "symmetric")) {
     if (value && !h->a_symmetric) return fail(h, MFODE_EINVAL, "symmetric mode needs A == A^T exactly");
+    if (value && h->flow == MFODE_FLOW_AFFINE)
+      return fail(h, MFODE_EINVAL, "symmetric mode needs every iterate to be a polynomial in A (not the affine flow)");
     if (value && h->small) h->small = false;   // K6 kernels compute full products
     h->sym = value != 0;
     return MFODE_OK;
@@ -1353,8 +1680,8 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     return MFODE_OK;
   }
   if (!strcmp(key, "small")) {
-    if (value && (h->n > kSmallMaxN || h->ms != 1))
-      return fail(h, MFODE_EINVAL, "small kernels need n <= %d and a one-matrix state", kSmallMaxN);
+    if (value && (h->n > kSmallMaxN || h->ms != 1 || h->flow == MFODE_FLOW_AFFINE))
+      return fail(h, MFODE_EINVAL, "small kernels need n <= %d, a one-matrix state and no source", kSmallMaxN);
     h->small = value != 0;
     return MFODE_OK;
   }
@@ -1395,14 +1722,14 @@ void mfode_destroy(mfode_ctx* h) {
     cudaFree(h->B);
   }
   if (h->stop_flag) cudaFree(h->stop_flag);
-  double* mbufs[] = {h->Qb, h->FQ, h->mtmp};
-  for (double* b : mbufs)
+  free_modified(h);
+  double* abufs[] = {h->Gsrc, h->X0dev};
+  for (double* b : abufs)
     if (b) {
-      forget_maps(b, b + state_elems(h) * (size_t)(h->bcap + 3));
+      oz_forget(b);
+      forget_maps(b, b + me);
       cudaFree(b);
     }
-  if (h->coef) cudaFree(h->coef);
-  if (h->mpart) cudaFree(h->mpart);
   if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
   delete h;
 }

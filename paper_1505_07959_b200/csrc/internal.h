@@ -23,6 +23,15 @@ struct Operand {
 };
 
 extern std::atomic<long long> g_launches;
+
+// Kernel attributes (max dynamic shared memory, occupancy) are per device: one-time set-up is
+// keyed by the current device ordinal (a process may drive several GPUs).
+constexpr int kMaxDevices = 64;
+inline int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
 extern bool g_pdl;   // programmatic dependent launch for the GEMM kernels (option "pdl")
 
 cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st);
@@ -43,6 +52,21 @@ cudaError_t launch_lincomb(double* out, const double* Q, long long qstride, cons
 cudaError_t launch_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide,
                             cudaStream_t st);
 cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, GemmParams p, cudaStream_t st);
+// Gram-Schmidt keep decision on the device (stats: two launch_frob mode-1 outputs, ||Z|| and r_ii)
+cudaError_t launch_gs_keep(double* Q, long long total, const double* stats, double tol, int* keep, cudaStream_t st);
+// D_i -= F0 for count states of stride `stride`
+cudaError_t launch_sub_bcast(double* D, long long stride, int count, const double* F0, long long total,
+                             cudaStream_t st);
+// out = ((sum_i coef[i] D_i + F0) + Gv) - G0   (Algorithm 4, eq. update2)
+cudaError_t launch_lincomb_affine(double* out, const double* D, long long qstride, const double* coef, int count,
+                                  long long total, const double* F0, const double* Gv, const double* G0,
+                                  cudaStream_t st);
+// out[0] = max over count states of ||X_i - Y_i||_F (0 if count == 0); partials >= 64 * count
+cudaError_t launch_frob_slices_max(const double* X, const double* Y, long long stride, int count, long long total,
+                                   double* partials, double* out, cudaStream_t st);
+// out = max_i *ptrs[i] / denom; stop flag = out <= tol (count <= 64)
+cudaError_t launch_max_ptrs(const double* const* ptrs, int count, double denom, double* out, double tol,
+                            int* stop_flag, cudaStream_t st);
 
 // f3(ii): FP64 GEMM emulated on the int8 tensor cores (ozaki.cu).  launch_gemm routes here when
 // p.oz_nmod > 0 (every epilogue except EPI_RESID).  Workspaces are per stream.

@@ -243,6 +243,123 @@ __global__ void k_axpy_dev(double* Y, const double* X, const double* coef, long 
   }
 }
 
+// ---- device-side Gram-Schmidt decision of Algorithm 2 (modified parareal) ----------
+// stats = [., ||Z_i||_F, ., r_ii] (two launch_frob mode-1 outputs).  Keep the block (reading R16)
+// iff r_ii > tol * max(1, ||Z_i||_F): Q_i = Q / r_ii; otherwise zero it, so later projections onto
+// this slot add exact zeros (the host compacts the basis once per sweep).  keep = 1 / 0, or -1 if
+// the candidate is not finite.
+__global__ void k_gs_keep(double* Q, long long total, const double* stats, double tol, int* keep) {
+  const double zn = stats[1], rii = stats[3];
+  const bool k = rii > tol * fmax(1.0, zn);
+  // -1: a non-finite candidate (reported as MFODE_ENONFINITE with its slice)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *keep = (isfinite(zn) && isfinite(rii)) ? (k ? 1 : 0) : -1;
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; e < total;
+       e += (long long)gridDim.x * blockDim.x * 2) {
+    double2 q = *reinterpret_cast<double2*>(Q + e);
+    if (k) {
+      q.x = q.x / rii;
+      q.y = q.y / rii;
+    } else {
+      q.x = 0.0;
+      q.y = 0.0;
+    }
+    *reinterpret_cast<double2*>(Q + e) = q;
+  }
+}
+
+// D_i = F(Q_i) - F(0) for `count` consecutive states (Algorithm 4, Remark P:424-428)
+__global__ void k_sub_bcast(double* D, long long stride, int count, const double* F0, long long total) {
+  for (int i = blockIdx.y; i < count; i += gridDim.y) {
+    double* d = D + (long long)i * stride;
+    for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; e < total;
+         e += (long long)gridDim.x * blockDim.x * 2) {
+      double2 v = *reinterpret_cast<double2*>(d + e);
+      const double2 f = *reinterpret_cast<const double2*>(F0 + e);
+      v.x = v.x - f.x;
+      v.y = v.y - f.y;
+      *reinterpret_cast<double2*>(d + e) = v;
+    }
+  }
+}
+
+// eq. (update2): out = ((sum_i coef[i] D_i + F0) + Gv) - G0  (ascending i)
+__global__ void k_lincomb_affine(double* out, const double* D, long long qstride, const double* coef, int count,
+                                 long long total, const double* F0, const double* Gv, const double* G0) {
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; e < total;
+       e += (long long)gridDim.x * blockDim.x * 2) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = 0; i < count; ++i) {
+      const double c = coef[i];
+      const double2 q = *reinterpret_cast<const double2*>(D + i * qstride + e);
+      s.x = fma(c, q.x, s.x);
+      s.y = fma(c, q.y, s.y);
+    }
+    const double2 f = *reinterpret_cast<const double2*>(F0 + e);
+    const double2 g = *reinterpret_cast<const double2*>(Gv + e);
+    const double2 g0 = *reinterpret_cast<const double2*>(G0 + e);
+    double2 r;
+    r.x = ((s.x + f.x) + g.x) - g0.x;
+    r.y = ((s.y + f.y) + g.y) - g0.y;
+    *reinterpret_cast<double2*>(out + e) = r;
+  }
+}
+
+// ---- SPEC stop rule: max_n ||X_n - Y_n||_F over `count` consecutive states -----------------
+constexpr int kSliceBlocks = 64;
+__global__ void __launch_bounds__(kRedThreads) k_frob_slices(const double* X, const double* Y, long long stride,
+                                                             long long total, double* partials) {
+  const double* x = X + (long long)blockIdx.y * stride;
+  const double* y = Y + (long long)blockIdx.y * stride;
+  double d = 0.0;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; i < total;
+       i += (long long)gridDim.x * blockDim.x * 2) {
+    const double2 a = *reinterpret_cast<const double2*>(x + i);
+    const double2 b = *reinterpret_cast<const double2*>(y + i);
+    const double e0 = a.x - b.x, e1 = a.y - b.y;
+    d = fma(e0, e0, d);
+    d = fma(e1, e1, d);
+  }
+  __shared__ double sd[kRedThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  if ((threadIdx.x & 31) == 0) sd[threadIdx.x >> 5] = d;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) a += sd[w];
+    partials[(long long)blockIdx.y * gridDim.x + blockIdx.x] = a;
+  }
+}
+
+// out = max over slices of sqrt(fixed-order sum of that slice's partials); count == 0 -> 0
+__global__ void k_reduce_slices_max(const double* partials, int count, int blocks, double* out) {
+  double best = 0.0;
+  for (int sl = 0; sl < count; ++sl) {
+    double a = (threadIdx.x < blocks) ? partials[(long long)sl * blocks + threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    __shared__ double s0[2];
+    if ((threadIdx.x & 31) == 0) s0[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) best = fmax(best, sqrt(s0[0] + s0[1]));
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = best;
+}
+
+// out = max_i vals[i][0] / denom; stop flag = (out <= tol)
+struct PtrList {
+  const double* p[64];
+  int count;
+};
+__global__ void k_max_ptrs(PtrList l, double denom, double* out, double tol, int* stop_flag) {
+  double m = 0.0;
+  for (int i = 0; i < l.count; ++i) m = fmax(m, *l.p[i]);
+  const double v = m / denom;
+  *out = v;
+  if (stop_flag) *stop_flag = (v <= tol) ? 1 : 0;
+}
+
 // --------------------------------------------------------------------------------------------
 // host wrappers
 // --------------------------------------------------------------------------------------------
@@ -306,6 +423,51 @@ cudaError_t launch_lincomb(double* out, const double* Q, long long qstride, cons
 cudaError_t launch_axpy_dev(double* Y, const double* X, const double* coef, long long total, int divide,
                             cudaStream_t st) {
   k_axpy_dev<<<ew_grid(total), 256, 0, st>>>(Y, X, coef, total, divide);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs_keep(double* Q, long long total, const double* stats, double tol, int* keep, cudaStream_t st) {
+  k_gs_keep<<<ew_grid(total), 256, 0, st>>>(Q, total, stats, tol, keep);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sub_bcast(double* D, long long stride, int count, const double* F0, long long total,
+                             cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int gx = std::max(1, ew_grid(total) / std::max(1, count));
+  k_sub_bcast<<<dim3(gx, std::min(count, 65535)), 256, 0, st>>>(D, stride, count, F0, total);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb_affine(double* out, const double* D, long long qstride, const double* coef, int count,
+                                  long long total, const double* F0, const double* Gv, const double* G0,
+                                  cudaStream_t st) {
+  k_lincomb_affine<<<ew_grid(total), 256, 0, st>>>(out, D, qstride, coef, count, total, F0, Gv, G0);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frob_slices_max(const double* X, const double* Y, long long stride, int count, long long total,
+                                   double* partials, double* out, cudaStream_t st) {
+  if (count > 0) {
+    k_frob_slices<<<dim3(kSliceBlocks, count), kRedThreads, 0, st>>>(X, Y, stride, total, partials);
+    ++g_launches;
+  }
+  k_reduce_slices_max<<<1, kSliceBlocks, 0, st>>>(partials, count, kSliceBlocks, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_ptrs(const double* const* ptrs, int count, double denom, double* out, double tol,
+                            int* stop_flag, cudaStream_t st) {
+  PtrList l;
+  if (count < 1 || count > 64) return cudaErrorInvalidValue;
+  for (int i = 0; i < count; ++i) l.p[i] = ptrs[i];
+  l.count = count;
+  k_max_ptrs<<<1, 1, 0, st>>>(l, denom, out, tol, stop_flag);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -389,29 +551,31 @@ void forget_maps(const double* lo, const double* hi) {
 // --------------------------------------------------------------------------------------------
 // GEMM dispatch
 // --------------------------------------------------------------------------------------------
-static int g_num_sms = 0;
 static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static int sms[kMaxDevices];
+  const int dev = cur_device();
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
   }
-  return g_num_sms;
+  return sms[dev];
 }
 
 template <int BM, int BN, int WM_, int WN_, int ST, int EPI>
 static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM_, WN_, ST>;
   auto kern = dgemm_tma_kernel<BM, BN, WM_, WN_, ST, EPI>;
-  static int occ = -1;
-  static std::once_flag once;
-  std::call_once(once, [&] {
+  static int occ_dev[kMaxDevices];
+  static std::once_flag once[kMaxDevices];
+  const int dev = cur_device();
+  std::call_once(once[dev], [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     int o = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads, Cfg::kSmemBytes);
-    occ = o > 0 ? o : 1;
+    occ_dev[dev] = o > 0 ? o : 1;
   });
+  const int occ = occ_dev[dev];
   const long long tm = (p.n + BM - 1) / BM;
   const long long tiles = ((BM == BN && p.sym) ? tm * (tm + 1) / 2 : tm * ((p.n + BN - 1) / BN)) * p.num_z;
   // Bounded persistence: a CTA owns at most ~2 ms of tiles.  Kernels are never preempted, so a grid
@@ -500,8 +664,8 @@ template <int NP>
 static cudaError_t fine_small_np(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
                                  long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st) {
   const size_t smem = 5 * SmallCfg<NP>::MAT * sizeof(double);
-  static std::once_flag once;
-  std::call_once(once, [&] {
+  static std::once_flag once[kMaxDevices];
+  std::call_once(once[cur_device()], [&] {
     cudaFuncSetAttribute(fine_smem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   fine_smem_kernel<NP><<<Z, kSmallThreads, smem, st>>>(flow, n, ld, M, Uin, Fout, mstride, mF, h, flag);
@@ -514,8 +678,8 @@ static cudaError_t coarse_small_np(int flow, int n, int ld, const double* M, con
                                    double* Gold, const double* Fk, long long mstride, int j0, int nloc, int mG,
                                    double h, int correct, cudaStream_t st) {
   const size_t smem = 4 * SmallCfg<NP>::MAT * sizeof(double);
-  static std::once_flag once;
-  std::call_once(once, [&] {
+  static std::once_flag once[kMaxDevices];
+  std::call_once(once[cur_device()], [&] {
     cudaFuncSetAttribute(coarse_smem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   coarse_smem_kernel<NP><<<1, kSmallThreads, smem, st>>>(flow, n, ld, M, Vin, U, Gold, Fk, mstride, j0, nloc, mG, h,

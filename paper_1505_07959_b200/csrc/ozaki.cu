@@ -921,14 +921,14 @@ static bool oz_map(CUtensorMap* m, const uint8_t* base, int n, int ldk, int coun
 }
 
 static int oz_num_sms() {
-  static int s = 0;
-  if (!s) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-    if (s <= 0) s = 148;
+  static int sms[kMaxDevices];
+  const int dev = cur_device();
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
   }
-  return s;
+  return sms[dev];
 }
 
 template <int EPI>
@@ -943,8 +943,8 @@ static cudaError_t launch_decode(const GemmParams& p, const uint16_t* R, long lo
 template <int PAIR>
 static cudaError_t launch_oz_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const OzGemmArgs& g, cudaStream_t st) {
   using Cfg = OzCfg<PAIR>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static std::once_flag once[kMaxDevices];
+  std::call_once(once[cur_device()], [] {
     cudaFuncSetAttribute(oz_gemm_kernel<PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (PAIR) cudaFuncSetAttribute(oz_gemm_kernel<PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   });

@@ -92,3 +92,28 @@ def test_no_oracle_import_in_product_path():
         if f.endswith(".py"):
             code = re.sub(r'"""[\s\S]*?"""|#.*', "", open(os.path.join(ROOT, "oracle", f)).read())
             assert "paper_1505_07959_b200" not in code and "mfode" not in code, f
+
+
+def test_affine_and_stop_rule_argument_checks_without_gpu():
+    L = mf.lib()
+    assert L.mfode_set_affine(None, None, None) == mf.EINVAL
+    assert L.mfode_modified_parareal_solve(None, 1, 0.0, 0, 0, None) == mf.EINVAL
+    assert mf.FLOW_AFFINE == 4 and mf.STOP_MAX_SLICE == 3
+    src = open(os.path.join(ROOT, "include", "mfode.h")).read()
+    assert "MFODE_FLOW_AFFINE = 4" in src and "MFODE_STOP_MAX_SLICE = 3" in src
+
+
+def test_kernel_wrappers_validate_operands_before_the_abi():
+    """a transposed view, a wrong dtype, a non-square or a host tensor must be
+    rejected by the binding -- the C ABI takes one leading dimension for every operand and TMA would
+    otherwise read past a smaller allocation."""
+    torch = pytest.importorskip("torch")
+    A = torch.zeros((8, 8), dtype=torch.float64)
+    with pytest.raises(ValueError, match="CUDA"):
+        mf.dgemm(A, A)
+    with pytest.raises(ValueError, match="CUDA"):
+        mf.frobenius(A)
+    with pytest.raises(ValueError):
+        mf.rk_stage(A, A, A, A, None, 1, 0.1)
+    with pytest.raises(ValueError, match="beta"):
+        mf.dgemm_emulated(A, A, beta=1.0)

@@ -561,3 +561,29 @@ def test_residual_definitions_closed_form():
     A = np.array([[4.0, 1.0], [0.0, 9.0]])
     assert dense.residual_sqrt(A, np.array([[2.0, 0.2], [0.0, 3.0]])) == 0.0
     assert dense.residual_sqrt(A, 2.0 * np.eye(2)) == pytest.approx(math.sqrt(26.0 / 98.0), rel=1e-15)
+
+
+def test_max_slice_stop_rule_against_binomial_closed_form():
+    """SPEC's stop rule (STOP_MAX_SLICE): stop at the first k with
+    max_n ||U^k_n - U^{k-1}_n||_F <= tol max(1, ||U_0||_F).  The expected k comes from the binomial
+    closed form of linear parareal (standard analysis, as test_linear_parareal_binomial_closed_form),
+    not from the oracle's own iterates; the metric values too."""
+    rng = np.random.default_rng(12)
+    n = 4
+    M = -np.eye(n) + 0.3 * rng.standard_normal((n, n))
+    X0 = 2.0 * np.eye(n) + 0.1 * rng.standard_normal((n, n))
+    T, N, mG, mF = 2.0, 8, 1, 6
+    hG, hF = T / (N * mG), T / (N * mF)
+    ZG, ZF = hG * M, hF * M
+    Gm = np.linalg.matrix_power(np.eye(n) + ZG, mG)
+    Fm = np.linalg.matrix_power(np.eye(n) + ZF + ZF @ ZF / 2 + ZF @ ZF @ ZF / 6 + ZF @ ZF @ ZF @ ZF / 24, mF)
+    U = lambda k, m: sum(math.comb(m, j) * np.linalg.matrix_power(Fm - Gm, j) @ np.linalg.matrix_power(Gm, m - j)
+                         for j in range(min(k, m) + 1)) @ X0
+    scale = max(1.0, np.linalg.norm(X0))
+    metric = [max(np.linalg.norm(U(k, m) - U(k - 1, m)) for m in range(N + 1)) / scale for k in range(1, N + 1)]
+    tol = math.sqrt(metric[2] * metric[3])          # strictly between sweeps 3 and 4
+    expect_k = next(k for k, v in enumerate(metric, start=1) if v <= tol)
+    assert expect_k == 4
+    out = dense.parareal(lambda X: M @ X, X0, T, N, mG, mF, N, tol, dense.STOP_MAX_SLICE)
+    assert out["k_done"] == expect_k and out["converged"]
+    np.testing.assert_allclose(out["deltas"], metric[:expect_k], rtol=1e-9)
