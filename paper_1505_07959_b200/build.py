@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmfode.so")
 SOURCES = ["kernels.cu", "ozaki.cu", "driver.cu"]
-HEADERS = ["gemm.cuh", "epilogue.cuh", "small.cuh", "ptx.cuh", "internal.h", "nccl_min.h", os.path.join("..", "..", "include", "mfode.h")]
+HEADERS = ["gemm.cuh", "fused.cuh", "epilogue.cuh", "small.cuh", "ptx.cuh", "internal.h", "nccl_min.h", os.path.join("..", "..", "include", "mfode.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]

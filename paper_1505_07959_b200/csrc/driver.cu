@@ -131,6 +131,7 @@ struct Rank {
   };
   std::vector<Span> spans;
   double* spart = nullptr;   // per-slice partial sums (MAX_SLICE stop test)
+  unsigned* sched = nullptr; // K10 fused fine kernel: ticket + per-slice counters (1 + cap)
 };
 
 }  // namespace mfode
@@ -159,6 +160,7 @@ struct mfode_ctx {
   double* Gsrc = nullptr;    // MFODE_FLOW_AFFINE: source G (device, zero by default)
   double* X0dev = nullptr;   // MFODE_FLOW_AFFINE: U_0 (device copy; identity by default)
   bool phase_timing = true;  // option "phase_timing"
+  int fused = -1;            // option "fused": K10 one-launch fine propagator (-1 auto, 0 off, 1 on)
   unsigned long long mat_gen = 0;   // content generation of A / B (emulated-GEMM encoding cache key)
   std::vector<mfode::Rank> ranks;
   // modified parareal (Algorithm 3): F-orthonormal basis Q of S^k, fine images F(Q), scratch
@@ -401,11 +403,46 @@ static int coarse_G(mfode_ctx* h, Rank& R, const double* in_slab, int in_count, 
 
 // Fine propagator F (m_F RK4 steps) on Z = jb - ja states, batched: input states ja.. of the slab
 // `in` (in_count states), output states ja.. of the slab `out` (out_count states), in place.
+// K10 (fused.cuh) serves moderate n with one-matrix states and plain FP64 GEMMs
+static bool use_fused(const mfode_ctx* h) {
+  const bool eligible = !h->small && !h->sym && h->oz_nmod == 0 && h->ms == 1 && h->flow != MFODE_FLOW_TRIG &&
+                        h->n <= kFusedMaxN;
+  if (h->fused == 0) return false;
+  if (h->fused == 1) return eligible;
+  return eligible && h->n > kSmallMaxN;
+}
+
 static int fine_prop(mfode_ctx* h, Rank& R, const double* in, int in_count, double* out, int out_count, int ja,
                      int jb, const int* stop_flag) {
   const int Z = jb - ja;
   const double hF = h->T / ((double)h->N * h->mF);
   const long long me = (long long)mat_elems(h);
+  if (use_fused(h)) {
+    if (Z > h->cap) return fail(h, MFODE_EINVAL, "fused fine batch %d exceeds capacity %d", Z, h->cap);
+    FusedLaunch L;
+    L.flow = h->flow;
+    L.n = h->n;
+    L.ld = h->ld;
+    L.Z = Z;
+    L.mF = h->mF;
+    L.ja = ja;
+    L.in_count = in_count;
+    L.out_count = out_count;
+    L.cap = h->cap;
+    L.h = hF;
+    L.M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
+    L.Cterm = (h->flow == MFODE_FLOW_SQRT) ? h->A : (h->flow == MFODE_FLOW_AFFINE ? h->Gsrc : nullptr);
+    L.in = in;
+    L.out = out;
+    L.Ya = R.Ya;
+    L.Yb = R.Yb;
+    L.W = R.W;
+    L.S = R.S;
+    L.stop_flag = stop_flag;
+    L.sched = R.sched;
+    CUDA_TRY(h, launch_fine_fused(L, R.fine));
+    return MFODE_OK;
+  }
   if (h->small) {
     const double* M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
     CUDA_TRY(h, launch_fine_small(h->flow, h->n, h->ld, M, in + (size_t)ja * state_elems(h),
@@ -457,7 +494,7 @@ static int fine_chunk(mfode_ctx* h, Rank& R, int par, int ja, int jb, const int*
 // rounds (tiles / concurrently resident CTAs, rounded up per launch) is minimal -- the last,
 // partial round of every launch is idle tensor time.  Ties go to larger chunks (fewer launches).
 static int fine_chunk_size(const mfode_ctx* h, int active) {
-  if (h->small || active <= 1) return std::max(1, std::min(active, h->cap));
+  if (h->small || use_fused(h) || active <= 1) return std::max(1, std::min(active, h->cap));
   const int tile = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, std::min(active, h->cap), h->sym);
   const long long t1 = gemm_tiles(tile, h->n, 1, h->sym) * h->ms;   // tiles of one slice's GEMM launch
   const long long slots = 148LL * (tile == TILE_128 ? 1 : (tile == TILE_64 ? 2 : 4));
@@ -513,7 +550,7 @@ static int enqueue_fine(mfode_ctx* h, Rank& R, int k, bool speculative) {
     }
     Rank::ChunkTiming& ct = R.tpool[R.tused++];
     ct.iter = k;
-    ct.launches = h->small ? 1 : h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
+    ct.launches = (h->small || use_fused(h)) ? 1 : h->mF * 4 * (h->flow == MFODE_FLOW_INVERSE ? 2 : 1);
     ct.flops = (double)(jb - ja) * h->mF * rk4_flops(h);
     if (h->sym && !h->small) {   // executed (not algorithmic) flops: only upper-triangle tiles run
       const int tl = (h->tile != TILE_AUTO) ? h->tile : choose_tile(h->n, (jb - ja) * h->ms, true);
@@ -609,6 +646,9 @@ static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
     TRY(send_boundary(h, R, nxt));
     return MFODE_OK;
   }
+  // K10: the fused fine sweep is one launch holding every SM, so no coarse GEMM can run beside it;
+  // wait for it here (outside the span) so that ms_correct stays the correction's own time
+  if (use_fused(h) && R.nloc > 0) CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, R.evF[R.chunk_of[R.nloc - 1]], 0));
   SpanCtx sc{&R, R.coarse, PH_CORRECT, -1};
   TRY(span_open(h, R, R.coarse, &sc.open));
   for (int j = j0; j < R.nloc; ++j) {
@@ -673,6 +713,7 @@ static int alloc_rank(mfode_ctx* h, Rank& R) {
   CUDA_TRY(h, cudaMalloc(&R.partials, sizeof(double) * (maxtiles + 16)));
   CUDA_TRY(h, cudaMalloc(&R.metric, sizeof(double) * 8));
   CUDA_TRY(h, cudaMalloc(&R.spart, sizeof(double) * 64 * (size_t)(R.nloc + 1)));
+  CUDA_TRY(h, cudaMalloc(&R.sched, sizeof(unsigned) * fused_sched_words(h->cap, std::min(h->n, kFusedMaxN))));
   CUDA_TRY(h, cudaMallocHost(&R.host_metric, sizeof(double) * 8));
   // zero everything once: padding columns stay zero forever (kernels never write them)
   CUDA_TRY(h, cudaMemset(R.U[0], 0, me * (R.nloc + 1)));
@@ -712,6 +753,7 @@ static void free_rank(mfode_ctx* h, Rank& R) {
       cudaFree(b);
     }
   if (R.host_metric) cudaFreeHost(R.host_metric);
+  if (R.sched) cudaFree(R.sched);
   if (R.fine) {
     cudaStreamSynchronize(R.fine);
     oz_release(R.fine);
@@ -1039,7 +1081,12 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
   int k_done = 0;
   bool converged = (stop == MFODE_STOP_FIXED_K);
   int status = MFODE_OK;
-  const bool spec = h->overlap && stop != MFODE_STOP_FIXED_K;
+  // Speculation (sweep k+1's fine work enqueued before the host reads sweep k's metric) pays when the
+  // fine sweep is chunked, so that chunk c can start as soon as the correction produced its inputs.
+  // The fused fine kernel (K10) is one persistent launch holding every SM: it cannot overlap the
+  // correction, and the metric kernel that would cancel it could not get an SM until it ends (a
+  // converged solve would pay one whole wasted sweep), so it runs strictly phased.
+  const bool spec = h->overlap && stop != MFODE_STOP_FIXED_K && !use_fused(h);
   if (K_eff > 0)
     for (auto& R : h->ranks) TRY(enqueue_fine(h, R, 0, false));
   for (int k = 0; k < K_eff; ++k) {
@@ -1639,6 +1686,11 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
   if (!h || !key) return set_global_err(MFODE_EINVAL, "NULL argument");
   if (!strcmp(key, "overlap")) {
     h->overlap = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "fused")) {   // K10 one-launch fine propagator: -1 auto (64 < n <= 512), 0 off, 1 on
+    if (value < -1 || value > 1) return fail(h, MFODE_EINVAL, "fused must be -1, 0 or 1");
+    h->fused = (int)value;
     return MFODE_OK;
   }
   if (!strcmp(key, "phase_timing")) {   // per-phase CUDA-event spans (mfode_solve_info ms_coarse ...)

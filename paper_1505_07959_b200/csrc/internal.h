@@ -93,6 +93,29 @@ void forget_maps(const double* lo, const double* hi);
 constexpr int kFrobPartials = 2 * 296;
 constexpr int kSmallMaxN = 64;   // K6 small-n persistent kernels handle n <= 64
 
+// K10: the whole fine propagator (m_F RK4 steps) of Z slices in one persistent launch (fused.cuh).
+// in/out: slabs of in_count/out_count states (the batch is states ja .. ja+Z-1 of both); Ya, Yb, S,
+// W (inverse flow only): scratch of `cap` states; M = B (inverse) or A; Cterm = A (sqrt), G (affine)
+// or null; sched: fused_sched_words(Z, n) unsigned counters (zeroed by the launcher).  flow: 0 inverse, 1 sqrt, 2 exp,
+// 4 affine (one-matrix states).
+constexpr int kFusedMaxN = 512;
+struct FusedLaunch {
+  int flow, n, ld, Z, mF, ja, in_count, out_count, cap;
+  double h;
+  const double* M;
+  const double* Cterm;
+  const double* in;
+  double *out, *Ya, *Yb, *W, *S;
+  const int* stop_flag;
+  unsigned* sched;
+};
+cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st);
+// scheduler words of a fused launch: the ticket + per slice rowK[tm], colK[tn], colW[tn] (64 x 64 tiles)
+inline size_t fused_sched_words(int Z, int n) {
+  const size_t t = (size_t)(n + 63) / 64;
+  return 1 + (size_t)Z * 3 * t;
+}
+
 // K6: all m_F RK4 steps of Z slices (one CTA each) in shared memory; M = B (inverse) or A (sqrt)
 cudaError_t launch_fine_small(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
                               long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st);

@@ -9,12 +9,14 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
 #include <algorithm>
 
+#include "fused.cuh"
 #include "gemm.cuh"
 #include "internal.h"
 #include "small.cuh"
@@ -655,6 +657,92 @@ cudaError_t launch_gemm(int epi, int tile, const Operand& A, const Operand& B, G
     case EPI_ACCEL: return dispatch_tile<EPI_ACCEL>(tile, ma, mb, p, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// --------------------------------------------------------------------------------------------
+// K10 fused fine propagator (fused.cuh)
+// --------------------------------------------------------------------------------------------
+template <int BM, int BN, int WM_, int WN_, int ST>
+static cudaError_t launch_fused_cfg(const FusedMaps& maps, const FusedParams& p, cudaStream_t st) {
+  using Cfg = GemmCfg<BM, BN, WM_, WN_, ST>;
+  auto kern = fine_fused_kernel<BM, BN, WM_, WN_, ST>;
+  constexpr int kSmem = Cfg::kSmemBytes + 8 * 8;   // + the tile-info ring
+  static int occ_dev[kMaxDevices];
+  static std::once_flag once[kMaxDevices];
+  const int dev = cur_device();
+  std::call_once(once[dev], [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads, kSmem);
+    occ_dev[dev] = o > 0 ? o : 1;
+  });
+  long long grid = (long long)num_sms() * occ_dev[dev];
+  if (grid > p.total) grid = p.total;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<long long>(1, grid));
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, maps, p);
+  ++g_launches;
+  return e;
+}
+
+cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st) {
+  // one tile config (64 x 64, 4 consumer warps, two or more CTAs per SM): the path serves n <= 512
+  constexpr int BM = 64, BN = 64;
+  const int n = L.n, ld = L.ld;
+  FusedMaps maps;
+  const int rows_a = BM;
+  if (!get_map(&maps.mA_M, L.M, n, ld, 1, rows_a) || !get_map(&maps.mA_in, L.in, n, ld, L.in_count, rows_a) ||
+      !get_map(&maps.mA_out, L.out, n, ld, L.out_count, rows_a) ||
+      !get_map(&maps.mA_ya, L.Ya, n, ld, L.cap, rows_a) || !get_map(&maps.mA_yb, L.Yb, n, ld, L.cap, rows_a) ||
+      !get_map(&maps.mB_in, L.in, n, ld, L.in_count, 16) || !get_map(&maps.mB_out, L.out, n, ld, L.out_count, 16) ||
+      !get_map(&maps.mB_ya, L.Ya, n, ld, L.cap, 16) || !get_map(&maps.mB_yb, L.Yb, n, ld, L.cap, 16))
+    return cudaErrorInvalidValue;
+  if (L.W) {
+    if (!get_map(&maps.mB_w, L.W, n, ld, L.cap, 16)) return cudaErrorInvalidValue;
+  } else {
+    maps.mB_w = maps.mB_ya;   // unused (only the inverse flow has a W phase)
+  }
+  const long long me = (long long)n * ld;
+  FusedParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = n;
+  p.ld = ld;
+  p.Z = L.Z;
+  p.mF = L.mF;
+  p.flow = L.flow;
+  p.gps = (L.flow == 0) ? 2 : 1;
+  p.tiles_n = (n + BN - 1) / BN;
+  p.tiles_m = (n + BM - 1) / BM;
+  p.T_tiles = p.tiles_m * p.tiles_n;
+  p.in_base = L.ja;
+  p.out_base = L.ja;
+  p.h = L.h;
+  p.Xin = MatRef{const_cast<double*>(L.in) + (size_t)L.ja * me, me};
+  p.Xout = MatRef{L.out + (size_t)L.ja * me, me};
+  p.Ya = MatRef{L.Ya, me};
+  p.Yb = MatRef{L.Yb, me};
+  p.W = MatRef{L.W, me};
+  p.S = MatRef{L.S, me};
+  p.Cterm = L.Cterm;
+  p.stop_flag = L.stop_flag;
+  p.sched = L.sched;
+  p.total = (long long)L.mF * 4 * p.gps * L.Z * p.T_tiles;
+  cudaError_t e = cudaMemsetAsync(L.sched, 0, sizeof(unsigned) * fused_sched_words(L.Z, n), st);
+  if (e != cudaSuccess) return e;
+  // Few tiles per phase (Z * T <= 2 per SM): one 8-consumer-warp CTA per SM finishes each tile twice
+  // as fast, shortening every slice's phase chain (the critical path); with more tiles, two 4-warp
+  // CTAs per SM overlap one CTA's dependency waits and epilogue with the other's main loop
+  // (measured, profiles/fused_r02.md).
+  if ((long long)L.Z * p.T_tiles <= 2LL * num_sms()) return launch_fused_cfg<BM, BN, 2, 4, 4>(maps, p, st);
+  return launch_fused_cfg<BM, BN, 2, 2, 4>(maps, p, st);
 }
 
 // --------------------------------------------------------------------------------------------

@@ -743,3 +743,75 @@ def test_cfg3_full_size_K1_vs_spectral_oracle():
     ref = spectral.reconstruct(w.eigvecs, sp["X"])
     assert relF(X, ref) <= 1e-10
     assert abs(info["deltas"][0] - sp["deltas"][0]) <= 1e-6 * sp["deltas"][0]
+
+
+# ---------------------------------------------------------------------------------------------
+# K10: the fused one-launch fine propagator (fused.cuh)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("flow,n", [(mf.FLOW_INVERSE, 100), (mf.FLOW_INVERSE, 256), (mf.FLOW_SQRT, 196),
+                                    (mf.FLOW_EXP, 130), (mf.FLOW_AFFINE, 120), (mf.FLOW_INVERSE, 300),
+                                    (mf.FLOW_INVERSE, 72)])
+def test_fused_fine_kernel_bitwise_equal_gemm_path(flow, n):
+    """K10 runs every RK4 phase of every slice of a sweep in one persistent launch (ticketed work
+    items, per-slice phase counters); its main loop and epilogues are the launch-per-GEMM path's,
+    so whole solves agree bitwise (ragged n: partial tiles in every phase), with far fewer launches;
+    both match the oracle."""
+    if flow == mf.FLOW_SQRT:
+        m = int(round(math.sqrt(n)))
+        A = workloads.laplacian_2d(m) + np.eye(m * m)
+        T, N, mG, mF, K, tol, stop = 20.0, 64, 2, 8, 3, 0.0, mf.STOP_FIXED_K
+    else:
+        A = workloads.random_spd(n, 40).A if flow != mf.FLOW_AFFINE else _affine_case(n, 40)[0]
+        T, N, mG, mF, K, tol, stop = 1.0, 7, 1, 6, 7, 1e-11, mf.STOP_DELTA
+    outs = []
+    for fused in (1, 0):
+        s = mf.Solver(A, flow, T, N, mG, mF)
+        if flow == mf.FLOW_AFFINE:
+            _, Gs, U0 = _affine_case(n, 40)
+            s.set_affine(Gs, U0)
+        s.set_option("fused", fused)
+        info = s.solve(K, tol, stop)
+        outs.append((info, s.result()))
+        s.close()
+    (i1, X1), (i0, X0) = outs
+    assert i1["k_done"] == i0["k_done"]
+    assert np.array_equal(X1, X0)
+    assert i1["deltas"] == i0["deltas"]
+    assert i1["gpu_launches"] < i0["gpu_launches"]
+    if flow == mf.FLOW_AFFINE:
+        _, Gs, U0 = _affine_case(n, 40)
+        ref = dense.solve(A, flow, T, N, mG, mF, K, tol, stop, source=Gs, X0=U0)
+    else:
+        ref = dense.solve(A, flow, T, N, mG, mF, K, tol, stop)
+    assert relF(X1, ref["X"]) <= 1e-12
+
+
+def test_fused_path_sequential_modified_and_ranks():
+    """K10 under every caller: sequential fine (K = N bitwise, P5), logical ranks (P9), the modified
+    parareal's batched fine images, and repeated tolerance solves (strictly phased: see solve_impl).  N = 24
+    slices of n = 256 (384 tiles per phase) run the two-CTAs-per-SM configuration, the sequential
+    runs (one slice) the 8-warp one."""
+    w = workloads.random_spd(256, 41)
+    N = 24
+    s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 8)
+    s.set_option("fused", 1)
+    s.solve(N)
+    XN = s.result()
+    s.sequential_fine()
+    assert np.array_equal(s.result(), XN)
+    ks = {s.solve(N, 1e-9, mf.STOP_DELTA)["k_done"] for _ in range(6)}
+    assert len(ks) == 1 and ks.pop() < N
+    X1 = s.result()
+    s3 = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 8, world=3)
+    s3.set_option("fused", 1)
+    s3.solve(N, 1e-9, mf.STOP_DELTA)
+    assert np.array_equal(s3.result(), X1)
+    se = mf.Solver(w.A, mf.FLOW_EXP, 1.0, N, 1, 8)
+    ie1 = se.solve_modified(3)
+    Xe1 = np.empty((256, 256))
+    se.result(Xe1)
+    se.set_option("fused", 0)
+    ie0 = se.solve_modified(3)
+    Xe0 = np.empty((256, 256))
+    se.result(Xe0)
+    assert ie1["basis_size"] == ie0["basis_size"] and np.array_equal(Xe1, Xe0)

@@ -45,6 +45,8 @@ def main():
                "fine_kernel_tflops": (i["fine_kernel_flops"] / (i["fine_kernel_ms"] * 1e-3) / 1e12
                                       if i["fine_kernel_ms"] > 0 else None),
                "launches_per_solve": i["gpu_launches"], "deltas": i["deltas"], "residual": s.residual(),
+               "phases_ms": {k: i[k] for k in ("ms_coarse", "ms_correct", "ms_comm", "ms_metric", "ms_fine",
+                                                "fine_kernel_ms")},
                "opts": args.opt}
         if args.seq:
             q = s.sequential_fine()
