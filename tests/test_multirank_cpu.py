@@ -115,3 +115,23 @@ def test_partitioned_schedule_bitwise(world):
     ref = dense.solve(w.A, dense.FLOW_INVERSE, *cfg[:5], tol=cfg[5], stop=cfg[6])
     assert k_done == ref["k_done"]
     assert np.array_equal(X, ref["X"])
+
+
+def test_bench_multi_gpu_request_fails_loudly_without_gpus():
+    """bench.py --gpus 2 outside torchrun re-launches itself as 2 ranks only when 2 GPUs are visible;
+    on a box with fewer it exits non-zero with a message instead of timing one rank."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 3
+    assert "--gpus 2" in r.stderr and "CUDA device" in r.stderr
+    # under torchrun the world size must match --gpus
+    env.update(WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 3 and "WORLD_SIZE=3" in r.stderr

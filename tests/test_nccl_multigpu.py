@@ -34,8 +34,10 @@ def _worker(rank, world, port, A, q):
     s = mf.Solver(A, mf.FLOW_INVERSE, 1.0, 8, 1, 8, world=world, rank=rank, device=rank, nccl_uid=obj[0])
     info = s.solve(8, 1e-12, mf.STOP_DELTA)
     X = s.result()
+    im = s.solve(8, 1e-9, mf.STOP_MAX_SLICE)          # SPEC stop: ncclAllReduce(max) of the slice metrics
+    Xm = s.result()
     if rank == 0:
-        q.put((info["k_done"], X))
+        q.put((info["k_done"], X, im["k_done"], Xm, info["ms_comm"]))
     s.close()
     dist.destroy_process_group()
 
@@ -50,18 +52,22 @@ def test_nccl_two_ranks_bitwise():
     s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, 8, 1, 8)
     i1 = s.solve(8, 1e-12, mf.STOP_DELTA)
     X1 = s.result()
+    im1 = s.solve(8, 1e-9, mf.STOP_MAX_SLICE)
+    Xm1 = s.result()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     ps = [ctx.Process(target=_worker, args=(r, 2, port, w.A, q)) for r in range(2)]
     for p in ps:
         p.start()
-    k, X = q.get(timeout=300)
+    k, X, km, Xm, ms_comm = q.get(timeout=300)
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
     assert k == i1["k_done"]
     assert np.array_equal(X, X1)
+    assert km == im1["k_done"] and np.array_equal(Xm, Xm1)
+    assert ms_comm > 0.0
 
 
 def test_nccl_one_rank_communicator_bitwise():
@@ -72,7 +78,8 @@ def test_nccl_one_rank_communicator_bitwise():
     import workloads
     w = workloads.random_spd(96, 5)
     for flow, T, N, mG, mF, K, tol, stop in ((mf.FLOW_INVERSE, 1.0, 8, 1, 8, 8, 1e-12, mf.STOP_DELTA),
-                                             (mf.FLOW_INVERSE, 1.0, 6, 1, 4, 3, 0.0, mf.STOP_FIXED_K)):
+                                             (mf.FLOW_INVERSE, 1.0, 6, 1, 4, 3, 0.0, mf.STOP_FIXED_K),
+                                             (mf.FLOW_INVERSE, 1.0, 8, 1, 8, 8, 1e-9, mf.STOP_MAX_SLICE)):
         s = mf.Solver(w.A, flow, T, N, mG, mF)
         i1 = s.solve(K, tol, stop)
         X1 = s.result()
