@@ -790,7 +790,7 @@ cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st) {
 template <int NP>
 static cudaError_t fine_small_np(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
                                  long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st) {
-  const size_t smem = 5 * SmallCfg<NP>::MAT * sizeof(double);
+  const size_t smem = 5 * SmallCfg<NP>::MAT * sizeof(double);   // M, X, Y_a, Y_b, W (S in registers)
   static std::once_flag once[kMaxDevices];
   std::call_once(once[cur_device()], [&] {
     cudaFuncSetAttribute(fine_smem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
