@@ -184,13 +184,40 @@ def cpu_baseline_line(w, d):
             "OMP_NUM_THREADS": d["OMP_NUM_THREADS"], "OPENBLAS_NUM_THREADS": d["OPENBLAS_NUM_THREADS"]}
 
 
+def plumbing_test(args):
+    """The multi-rank harness of the bench without a GPU (tests/test_multirank_cpu.py): gloo process
+    group, barrier, each rank times a token amount of host work, the max over ranks is reduced to rank 0,
+    which prints one JSON line with n_gpus = WORLD_SIZE and the per-rank slice blocks."""
+    import torch
+    import torch.distributed as dist
+    import paper_1505_07959_b200 as mf
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"plumbing_test": True, "n_gpus": world, "max_rank_ms": float(t.item()),
+                          "rank_slice_blocks": [list(mf.partition(64, world, r)) for r in range(world)]}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def spawn_ranks(args):
     """--gpus N without a torchrun environment: re-launch this script as N ranks (one per GPU,
     torch.distributed.run on 127.0.0.1).  Fails loudly when the box has fewer than N GPUs."""
     import socket
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and not args.plumbing_test:
         print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible", file=sys.stderr)
         return 3
     with socket.socket() as sock:
@@ -215,11 +242,17 @@ def main():
                     help="timed solves of the f3(ii) int8-tensor-core emulated variant (0: skip)")
     ap.add_argument("--emu-moduli", type=int, default=16)
     ap.add_argument("--no-seqfine", action="store_true", help="skip timing mfode_sequential_fine (the K = N reference)")
+    ap.add_argument("--no-secondary", dest="secondary", action="store_false",
+                    help="skip the cfg[0] / cfg[1] iteration-dynamics lines reported beside the headline")
+    ap.add_argument("--plumbing-test", action="store_true",
+                    help="CPU check of the multi-rank plumbing (spawn, gloo barrier, max over ranks); no solve")
     args = ap.parse_args()
 
     in_torchrun = "WORLD_SIZE" in os.environ
     if not in_torchrun and args.gpus > 1 and args.impl == "mine":
         return spawn_ranks(args)
+    if args.plumbing_test:
+        return plumbing_test(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -393,6 +426,29 @@ def main():
     emu_sym = (variant({"emulation": args.emu_moduli, "symmetric": 1}, args.emu_steps)
                if args.emu_steps > 0 else None)
 
+    # The headline config converges at k = 1 (one fine sweep); the smaller BASELINE configs exercise
+    # the iteration (k_done 4 and 6) on the other fine-propagator kernels (K6 at n = 32, K10 at
+    # n = 256).  Reported beside the headline, one GPU (rank 0 alone), not folded into `value`.
+    secondary = None
+    if world == 1 and args.secondary:
+        secondary = []
+        for c in (0, 1):
+            wc = workloads.config(c, with_eig=False)
+            sc = mf.Solver(wc.A, wc.flow, wc.T, wc.N, wc.m_G, wc.m_F)
+            sc.solve(wc.K_max, wc.tol, wc.stop)   # warm-up
+            ic = [sc.solve(wc.K_max, wc.tol, wc.stop) for _ in range(3)]
+            ms = float(np.mean([i["ms_total"] for i in ic]))
+            sq = sc.sequential_fine()
+            kf = ic[-1]
+            secondary.append({
+                "workload": wc.name, "n": wc.n, "N_slices": wc.N, "k_done": kf["k_done"],
+                "time_to_tol_ms": ms, "fine_tflops_whole_solve": kf["fine_flops"] / (ms * 1e-3) / 1e12,
+                "fine_kernel_tflops": kf["fine_kernel_flops"] / (kf["fine_kernel_ms"] * 1e-3) / 1e12,
+                "fine_kernel": "K6 fine_smem_kernel" if wc.n <= 64 else "K10 fine_fused_kernel",
+                "gpu_launches_per_solve": kf["gpu_launches"], "sequential_fine_ms": sq["ms_total"],
+                "speedup_vs_sequential_fine": sq["ms_total"] / ms})
+            sc.close()
+
     # the K = N reference: sequential fine propagation through the same ranks (the
     # same work as one GPU: each rank propagates its slices in turn and hands the state on)
     seq = None
@@ -458,6 +514,7 @@ def main():
             "f3_symmetric_variant": sym,
             "f3_emulated_variant": emu,
             "f3_emulated_symmetric_variant": emu_sym,
+            "secondary_configs": secondary,
         }
         print(json.dumps(line), flush=True)
     solver.close()

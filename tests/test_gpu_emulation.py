@@ -331,3 +331,25 @@ def test_emulated_gemm_extreme_row_scales():
     rowerr = np.abs(D - ref).max(1) / np.abs(ref).max(1)
     assert rowerr.max() <= 1e-13
     assert np.abs(D[:, 5] - ref[:, 5]).max() <= 1e-13 * np.abs(ref[:, 5]).max()
+
+
+def test_emulated_gemm_graded_rows_normwise_accuracy():
+    """the emulation scales each row of A (column of B) by its largest entry, so its error
+    bound is NORMWISE per row/column (include/mfode.h), not elementwise-relative.  With entries inside
+    each row spanning 8 decades of the row maximum, every element stays within that bound, the result
+    is FP64-accurate relative to |A||B| (what the bound promises), and entries much smaller than their
+    row maximum lose relative accuracy -- measured here, not hidden."""
+    n, nmod = 256, 16
+    rng = np.random.default_rng(77)
+    grade = 10.0 ** rng.uniform(-8, 0, (n, n))              # |A_ik| spans 1e-8 .. 1 of the row max
+    A = rng.standard_normal((n, n)) * grade
+    B = rng.standard_normal((n, n)) * 10.0 ** rng.uniform(-8, 0, (n, n))
+    D = mf.dgemm_emulated(_dev(A), _dev(B), n_moduli=nmod).cpu().numpy()
+    ref = A @ B
+    err = np.abs(D - ref)
+    assert np.all(err <= emu_bound(A, B, abits(nmod, n)))
+    scale = np.abs(A) @ np.abs(B)
+    assert np.max(err / scale) <= 4 * n * U53                 # normwise: FP64-level against |A||B|
+    # the same product on the FP64 DMMA path for contrast: also within gamma_n |A||B| (bitwise different)
+    Dd = mf.dgemm(_dev(A), _dev(B)).cpu().numpy()
+    assert np.max(np.abs(Dd - ref) / scale) <= 2 * n * U53

@@ -135,3 +135,25 @@ def test_bench_multi_gpu_request_fails_loudly_without_gpus():
     r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0",
                         "--no-cpu-baseline"], capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 3 and "WORLD_SIZE=3" in r.stderr
+
+
+def test_bench_spawn_path_with_gloo():
+    """bench.py --gpus 2 re-launches itself as two ranks through torch.distributed.run; the plumbing
+    test mode runs that path on CPU with gloo: barrier, max over ranks, rank 0 prints one line with
+    n_gpus = 2 and the contiguous slice blocks (the spawn path is checked with gloo)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--plumbing-test"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["rank_slice_blocks"] == [[0, 32], [32, 32]]
+    assert d["max_rank_ms"] >= 19.0      # rank 1 sleeps 20 ms: the max over ranks, not rank 0's time
