@@ -194,9 +194,7 @@ MFODE_API int mfode_get_slice(mfode_ctx *h, int n_index, double *U);
  * moduli, see mfode_dgemm_emulated; EINVAL if n leaves fewer than 8 bits per operand).  Process-wide
  * keys (they affect every handle of the process): "pdl" (1 = programmatic dependent launch of
  * consecutive GEMMs, default; 0 = plain stream order), "oz_pair" (1 = CTA-pair int8 GEMM kernel,
- * default; 0 = single-CTA kernel; results are bitwise identical), "dyn_sched" (1 = the DMMA GEMM's tiles
- * are handed out by a per-stream atomic ticket, default; 0 = static round-robin; bitwise identical).
- * Per handle also: "fused" (-1 = auto: the one-launch fine propagator K10 for 64 < n <= 512, 0 = off,
+ * default; 0 = single-CTA kernel; results are bitwise identical).  Per handle also: "fused" (-1 = auto: the one-launch fine propagator K10 for 64 < n <= 512, 0 = off,
  * 1 = on where eligible; bitwise identical) and "phase_timing" (1 = per-phase CUDA-event spans in
  * mfode_solve_info, default; 0 = off). */
 MFODE_API int mfode_set_option(mfode_ctx *h, const char *key, int64_t value);

@@ -757,13 +757,11 @@ static void free_rank(mfode_ctx* h, Rank& R) {
   if (R.fine) {
     cudaStreamSynchronize(R.fine);
     oz_release(R.fine);
-    sched_release(R.fine);
     cudaStreamDestroy(R.fine);
   }
   if (R.coarse) {
     cudaStreamSynchronize(R.coarse);
     oz_release(R.coarse);
-    sched_release(R.coarse);
     cudaStreamDestroy(R.coarse);
   }
   for (auto e : R.evC) cudaEventDestroy(e);
@@ -1733,10 +1731,6 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     g_pdl = value != 0;
     return MFODE_OK;
   }
-  if (!strcmp(key, "dyn_sched")) {   // process-wide: ticketed (1, default) or round-robin (0) GEMM tiles
-    g_dyn_sched = value != 0;
-    return MFODE_OK;
-  }
   if (!strcmp(key, "small")) {
     if (value && (h->n > kSmallMaxN || h->ms != 1 || h->flow == MFODE_FLOW_AFFINE))
       return fail(h, MFODE_EINVAL, "small kernels need n <= %d, a one-matrix state and no source", kSmallMaxN);
@@ -1839,7 +1833,6 @@ int mfode_dgemm_emulated(const double* dA, const double* dB, const double* dC, d
 int mfode_release_workspace(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   oz_release((cudaStream_t)stream);
-  sched_release((cudaStream_t)stream);
   if (e != cudaSuccess) return set_global_err(MFODE_ECUDA, "release_workspace: %s", cudaGetErrorString(e));
   return MFODE_OK;
 }

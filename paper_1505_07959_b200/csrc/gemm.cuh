@@ -15,10 +15,7 @@
 //
 // FP64 on B200 has no tcgen05 kind (ptxas rejects kind::f64) and no wgmma, so the tensor path is
 // warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, measured 37.0 TF/s chip peak).  Structure:
-//   * persistent CTAs over (z, grouped tile raster); tiles are handed out by a per-stream atomic
-//     ticket (dynamic: a CTA that starts late, e.g. behind the coarse stream's or NCCL's kernels,
-//     simply takes fewer tiles) or, without a ticket buffer, round-robin; each tile's k order is
-//     fixed, so either schedule gives bitwise the same results;
+//   * persistent CTAs, static round-robin tile schedule over (z, grouped tile raster);
 //   * one producer warp: one elected lane issues cp.async.bulk.tensor (TMA) loads of a
 //     BM x 16 A tile and BN/16 16x16 B boxes per k-step into a STAGES-deep mbarrier ring,
 //     128B swizzle (so fragment loads are bank-conflict free, see below);
@@ -68,8 +65,6 @@ struct GemmParams {
   const int* stop_flag;   // if non-null and set: the launch does nothing
   int oz_reuse_left;      // emulated GEMM: A == the previous launch's right operand, unchanged (ozaki.cu)
   int oz_nmod;            // > 0: emulated FP64 GEMM on the int8 tensor cores with this many moduli (ozaki.cu)
-  unsigned* sched;        // non-null: dynamic tile schedule, [0] ticket, [1] exited CTAs (per stream,
-                          // zero at launch; the last CTA to exit resets both); null: static round-robin
 };
 
 }  // namespace mfode
@@ -99,26 +94,13 @@ struct GemmCfg {
   // which the mirrored elements are written as 64-byte row segments
   static constexpr int kMirrorPitch = 33;
   static constexpr int kMirrorDoubles = (BM == BN) ? kConsumerWarps * 2 * 8 * kMirrorPitch : 0;
-  static constexpr int kTileRing = 8;   // tile indices handed from the producer to the consumers
   static constexpr int kSmemBytes =
-      STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8 + kMirrorDoubles * 8 + kTileRing * 4;
+      STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8 + kMirrorDoubles * 8;
   static_assert(WM % 8 == 0 && WN % 16 == 0, "warp tile must be a multiple of 8 x 16");
   static_assert(BM <= 256 && BN % 16 == 0, "TMA box limits");
 };
 
 __device__ __forceinline__ int rho8(int g) { return ((g & 1) << 2) | (g >> 1); }
-
-// Dynamic tile schedule bookkeeping: a CTA that has taken its last ticket counts itself out; the last
-// one resets the ticket and the count, so the buffer is zero again for the next launch on the stream
-// (which touches it only after griddepcontrol.wait, i.e. after this grid has completed).
-__device__ __forceinline__ void sched_cta_exit(unsigned* sched) {
-  unsigned prev;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(sched + 1) : "memory");
-  if (prev == gridDim.x - 1) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(sched) : "memory");
-    asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(sched + 1) : "memory");
-  }
-}
 
 // tile index r -> (tile_m, tile_n): grouped raster, or over the upper triangle tile_m <= tile_n (sym).
 // The grouped raster walks column-major inside bands of kGroupM tile rows, so the ~148 tiles in
@@ -156,9 +138,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   uint64_t* empty = full + STAGES;
   double* red = reinterpret_cast<double*>(empty + STAGES);   // EPI_RESID cross-warp scratch
   double* mirror_stage = red + 64;                            // symmetric-mode mirror staging
-  int* tring = reinterpret_cast<int*>(mirror_stage + Cfg::kMirrorDoubles);   // tile ring (-1: no more tiles)
-  static_assert(STAGES < Cfg::kTileRing && (Cfg::kTileRing & (Cfg::kTileRing - 1)) == 0,
-                "the producer runs at most STAGES tiles ahead; the ring size is a power of two");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -184,10 +163,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   // the previous grid (all of its writes visible) before touching global memory.
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (cta_stop(p.stop_flag)) {
-    if (p.sched && threadIdx.x == 0) sched_cta_exit(p.sched);
-    return;
-  }
+  if (cta_stop(p.stop_flag)) return;
 
   if constexpr (Cfg::kSetMaxNReg) {
     if (warp >= Cfg::kConsumerWarps)
@@ -203,19 +179,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
       tma_prefetch_desc(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      // Bounded persistence: at most ceil(total / grid) tiles per CTA (about 2 ms, launch_cfg), so
-      // CTAs retire through the launch and the high-priority coarse stream's CTAs get SMs.
-      const int cap = (total + (int)gridDim.x - 1) / (int)gridDim.x;
-      for (int seq = 0;; ++seq) {
-        int t = total;
-        if (seq < cap) t = p.sched ? (int)atomicAdd(p.sched, 1u) : (int)(blockIdx.x + (long long)seq * gridDim.x);
-        if (t >= total) {   // no more tiles: wake the consumers on the next stage without data
-          mbar_wait(&empty[stage], phase ^ 1);
-          tring[seq % Cfg::kTileRing] = -1;
-          mbar_arrive(&full[stage]);
-          if (p.sched) sched_cta_exit(p.sched);
-          break;
-        }
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int z = t / tiles_per_z;
         const int r = t - z * tiles_per_z;
         int tm_, tn_;
@@ -252,7 +216,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
             }
           }
           mbar_wait(&empty[stage], phase ^ 1);
-          if (kt == 0) tring[seq % Cfg::kTileRing] = t;   // published by the arrive below (release.cta)
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
           unsigned char* sB = sA + Cfg::kABytes;
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
@@ -276,10 +239,14 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   uint32_t phase = 0;
   const uint32_t smem_base = smem_u32(smem);
 
-  for (int ri = 0;; ri = (ri + 1) & (Cfg::kTileRing - 1)) {
-    mbar_wait(&full[stage], phase);   // the tile's first stage (or the no-more-tiles signal)
-    const int t = tring[ri];
-    if (t < 0) break;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int z = t / tiles_per_z;
+    const int r = t - z * tiles_per_z;
+    int tm_, tn_;
+    tile_coords(sym, r, tiles_m, tiles_n, tm_, tn_);
+    const int m0 = tm_ * BM;
+    const int n0 = tn_ * BN;
+    const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
 
     double acc[Cfg::MT][2 * Cfg::NG][2];
 #pragma unroll
@@ -287,7 +254,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
 #pragma unroll
       for (int j = 0; j < 2 * Cfg::NG; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    bool ready = true;    // full[stage] already observed complete (above, or by the early probe)
+    bool ready = false;   // full[stage] already observed complete by the early probe
     for (int kt = 0; kt < KT; ++kt) {
       if (!ready) mbar_wait(&full[stage], phase);
       const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
@@ -339,14 +306,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     }
 
     // ---------------- epilogue ----------------
-    // tile coordinates only now: nothing of them is live across the main loop (register budget)
-    const int z = t / tiles_per_z;
-    const int r = t - z * tiles_per_z;
-    int tm_, tn_;
-    tile_coords(sym, r, tiles_m, tiles_n, tm_, tn_);
-    const int m0 = tm_ * BM;
-    const int n0 = tn_ * BN;
-    const double alpha = (p.alt_sign && (z & 1)) ? -p.alpha : p.alpha;
     double part = 0.0;
     const int ld = p.ld;
     if constexpr (EPI != EPI_RESID && BM == BN) {

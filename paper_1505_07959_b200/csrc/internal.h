@@ -33,8 +33,6 @@ inline int cur_device() {
   return dev;
 }
 extern bool g_pdl;   // programmatic dependent launch for the GEMM kernels (option "pdl")
-extern bool g_dyn_sched;   // dynamic (ticketed) tile schedule of the DMMA GEMM (option "dyn_sched")
-void sched_release(cudaStream_t st);   // free the stream's tile-schedule words
 
 cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st);
 cudaError_t launch_i_minus(double* B, const double* A, int n, int ld, cudaStream_t st);

@@ -25,42 +25,6 @@ namespace mfode {
 
 std::atomic<long long> g_launches{0};
 bool g_pdl = true;
-bool g_dyn_sched = true;
-
-// Per-(device, stream) dynamic tile-schedule words of the DMMA GEMM (gemm.cuh): zero at every launch
-// boundary (the last CTA of a grid resets them), so one buffer serves every launch on its stream.
-struct SchedCache {
-  std::mutex mu;
-  std::map<std::pair<int, cudaStream_t>, unsigned*> bufs;
-};
-static SchedCache& sched_cache() {
-  static SchedCache c;
-  return c;
-}
-static unsigned* stream_sched(cudaStream_t st) {
-  auto& c = sched_cache();
-  std::lock_guard<std::mutex> lk(c.mu);
-  const auto key = std::make_pair(cur_device(), st);
-  auto it = c.bufs.find(key);
-  if (it != c.bufs.end()) return it->second;
-  unsigned* b = nullptr;
-  if (cudaMalloc(&b, 2 * sizeof(unsigned)) != cudaSuccess) return nullptr;
-  if (cudaMemset(b, 0, 2 * sizeof(unsigned)) != cudaSuccess) {
-    cudaFree(b);
-    return nullptr;
-  }
-  c.bufs[key] = b;
-  return b;
-}
-void sched_release(cudaStream_t st) {
-  auto& c = sched_cache();
-  std::lock_guard<std::mutex> lk(c.mu);
-  const auto key = std::make_pair(cur_device(), st);
-  auto it = c.bufs.find(key);
-  if (it == c.bufs.end()) return;
-  cudaFree(it->second);
-  c.bufs.erase(it);
-}
 
 // --------------------------------------------------------------------------------------------
 // Element-wise kernels (HBM-bound; 16-byte vector accesses; padding columns kept at zero)
@@ -621,15 +585,14 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
   // stream (the sequential critical path); retiring CTAs every ~2 ms lets its CTAs in.
   const double tile_s = 2.0 * BM * BN * (double)p.n / (37e12 / (num_sms() * occ));
   const long long max_tiles_per_cta = std::max<long long>(1, (long long)(2e-3 / tile_s));
-  // The grid is a whole number of waves (a multiple of the resident-CTA slots) and every CTA takes at
-  // most ceil(tiles / grid) tiles (round-robin, or by the dynamic ticket, which lets CTAs that start
-  // late -- behind coarse-stream or NCCL kernels -- take fewer).
+  // The grid is a whole number of waves (a multiple of the resident-CTA slots), so the static
+  // round-robin gives every CTA floor/ceil(tiles / grid) tiles and no wave is left half empty.
+  // (A per-stream atomic tile ticket was built in round 2 and measured 1.3 % slower on this kernel,
+  // in its static form too -- profiles/ab_dyn_sched_regression_r02_*.jsonl -- so it was removed.)
   const long long slots = (long long)num_sms() * occ;
   const long long waves = std::max<long long>(1, (tiles + slots * max_tiles_per_cta - 1) / (slots * max_tiles_per_cta));
   long long grid = slots * waves;
   if (grid > tiles) grid = tiles;
-  GemmParams q = p;
-  q.sched = g_dyn_sched ? stream_sched(st) : nullptr;
   // Programmatic dependent launch: this grid may be scheduled while the previous kernel of the
   // stream drains; the kernel's griddepcontrol.wait orders every global access after it.
   cudaLaunchConfig_t cfg = {};
@@ -642,7 +605,7 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, q);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
   ++g_launches;
   return e;
 }
