@@ -12,10 +12,11 @@ import numpy as np, torch
 import paper_1505_07959_b200 as mf
 import workloads
 torch.cuda.set_device(0)
-if len(sys.argv) > 3 and sys.argv[3] != "-":   # process-wide option, when the build knows it
+if len(sys.argv) > 3 and sys.argv[3] != "-":   # process-wide option key=value, when the build knows it
     _s = mf.Solver(np.eye(8), mf.FLOW_INVERSE, 1.0, 2, 1, 1)
+    _k, _v = sys.argv[3].split("=")
     try:
-        _s.set_option("dyn_sched", int(sys.argv[3]))
+        _s.set_option(_k, int(_v))
     except Exception:
         pass
     _s.close()
