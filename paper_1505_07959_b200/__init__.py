@@ -140,6 +140,26 @@ def _ptr(x) -> Optional[int]:
     return x.data_ptr()
 
 
+def _host_square(M, n: int, name: str, rows: Optional[int] = None) -> np.ndarray:
+    """A C-contiguous float64 host copy of M with shape (rows or n, n), else ValueError (raw pointers
+    cross the ABI: a wrong shape would make the library read or write past the buffer)."""
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    want = (rows if rows is not None else n, n)
+    if M.shape != want:
+        raise ValueError(f"{name} must have shape {want}, got {M.shape}")
+    return M
+
+
+def _host_out(out, shape, name: str) -> np.ndarray:
+    """Validate (or allocate) a host output buffer written by the library."""
+    if out is None:
+        return np.empty(shape, dtype=np.float64)
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64 or not out.flags.c_contiguous \
+            or not out.flags.writeable or out.shape != tuple(shape):
+        raise ValueError(f"{name} must be a writable C-contiguous float64 array of shape {tuple(shape)}")
+    return out
+
+
 def _stream_ptr(stream) -> Optional[int]:
     if stream is None:
         return None
@@ -174,16 +194,21 @@ class Solver:
             dist = Dist(rank, world, device, uid_p)
         if isinstance(A, np.ndarray):
             A = np.ascontiguousarray(A, dtype=np.float64)
+            if A.ndim != 2 or A.shape[0] != A.shape[1]:
+                raise ValueError(f"A must be square, got shape {A.shape}")
             self.n = A.shape[0]
             st = L.mfode_create(ctypes.byref(self._h), A.ctypes.data, self.n, flow, T, N, m_G, m_F,
                                 ctypes.byref(dist) if dist else None)
         else:   # torch CUDA tensor
-            assert A.is_cuda and A.dtype.__str__() == "torch.float64" and A.is_contiguous()
+            if not (getattr(A, "is_cuda", False) and str(A.dtype) == "torch.float64" and A.is_contiguous()
+                    and A.dim() == 2 and A.shape[0] == A.shape[1]):
+                raise ValueError("A must be a numpy array or a square, contiguous CUDA float64 tensor")
             self.n = A.shape[0]
             st = L.mfode_create_device(ctypes.byref(self._h), A.data_ptr(), self.n, flow, T, N, m_G, m_F,
                                        ctypes.byref(dist) if dist else None, _stream_ptr(stream))
         _check(st)
         self.flow, self.T, self.N, self.m_G, self.m_F, self.world = flow, T, N, m_G, m_F, world
+        self.state_rows = 2 * self.n if flow == FLOW_TRIG else self.n   # the trig state is (sin; cos)
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -203,19 +228,13 @@ class Solver:
         self.close()
 
     def set_matrix(self, A: np.ndarray):
-        A = np.ascontiguousarray(A, dtype=np.float64)
-        assert A.shape == (self.n, self.n)
+        A = _host_square(A, self.n, "A")
         _check(lib().mfode_set_matrix(self._h, A.ctypes.data), self._h)
 
     def set_affine(self, G: Optional[np.ndarray] = None, U0: Optional[np.ndarray] = None):
         """FLOW_AFFINE: source G (None = 0) and initial state U0 (None = I) (mfode_set_affine)."""
-        def host(M):
-            if M is None:
-                return None
-            M = np.ascontiguousarray(M, dtype=np.float64)
-            assert M.shape == (self.n, self.n)
-            return M
-        G, U0 = host(G), host(U0)
+        G = None if G is None else _host_square(G, self.n, "G")
+        U0 = None if U0 is None else _host_square(U0, self.n, "U0")
         _check(lib().mfode_set_affine(self._h, _ptr(G), _ptr(U0)), self._h)
 
     def set_option(self, key: str, value: int):
@@ -248,17 +267,20 @@ class Solver:
         return r.value
 
     def result(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        if out is None:
-            out = np.empty((self.n, self.n), dtype=np.float64)
+        """U_N on the host: n x n, or 2n x n (sin; cos) for the trig flow."""
+        out = _host_out(out, (self.state_rows, self.n), "out")
         _check(lib().mfode_get_result(self._h, out.ctypes.data), self._h)
         return out
 
     def result_device(self, out, stream=None):
+        if not (getattr(out, "is_cuda", False) and str(out.dtype) == "torch.float64" and out.is_contiguous()
+                and tuple(out.shape) == (self.state_rows, self.n)):
+            raise ValueError(f"out must be a contiguous CUDA float64 tensor of shape {(self.state_rows, self.n)}")
         _check(lib().mfode_get_result_device(self._h, out.data_ptr(), _stream_ptr(stream)), self._h)
         return out
 
-    def slice(self, n_index: int) -> np.ndarray:
-        out = np.empty((self.n, self.n), dtype=np.float64)
+    def slice(self, n_index: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        out = _host_out(out, (self.state_rows, self.n), "out")
         _check(lib().mfode_get_slice(self._h, n_index, out.ctypes.data), self._h)
         return out
 
@@ -359,6 +381,7 @@ def cosine(A: np.ndarray, N: int, m_G: int, m_F: int, K_max: int, tol: float = 0
     """Algorithm 5 through mfode_cosine: returns (cos(A), m, info)."""
     A = np.ascontiguousarray(A, dtype=np.float64)
     n = A.shape[0]
+    A = _host_square(A, n, "A")
     C = np.empty((n, n), dtype=np.float64)
     m = ctypes.c_int()
     info = SolveInfo()
@@ -374,9 +397,10 @@ def accel_inverse(A: np.ndarray, E0: Optional[np.ndarray], dt: float, max_steps:
     """Algorithm 8 through mfode_accel_inverse: returns (X, steps, residual, status)."""
     A = np.ascontiguousarray(A, dtype=np.float64)
     n = A.shape[0]
+    A = _host_square(A, n, "A")
     X = np.empty((n, n), dtype=np.float64)
-    E0 = None if E0 is None else np.ascontiguousarray(E0, dtype=np.float64)
-    X0 = None if X0 is None else np.ascontiguousarray(X0, dtype=np.float64)
+    E0 = None if E0 is None else _host_square(E0, n, "E0")
+    X0 = None if X0 is None else _host_square(X0, n, "X0")
     steps, res = ctypes.c_int(), ctypes.c_double()
     st = _check(lib().mfode_accel_inverse(A.ctypes.data, _ptr(X0), _ptr(E0), n, dt, max_steps, tol, check_every,
                                           X.ctypes.data, ctypes.byref(steps), ctypes.byref(res)))

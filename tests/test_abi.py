@@ -117,3 +117,20 @@ def test_kernel_wrappers_validate_operands_before_the_abi():
         mf.rk_stage(A, A, A, A, None, 1, 0.1)
     with pytest.raises(ValueError, match="beta"):
         mf.dgemm_emulated(A, A, beta=1.0)
+
+
+def test_host_buffers_validated_before_the_abi():
+    """Host arrays that the library reads or writes through raw pointers are shape-checked in the
+    binding (a smaller buffer would be overrun): result / slice outputs (2n x n for the trig flow),
+    set_matrix / set_affine / accel_inverse inputs."""
+    with pytest.raises(ValueError):
+        mf._host_out(np.empty((3, 4)), (4, 4), "out")
+    with pytest.raises(ValueError):
+        mf._host_out(np.empty((4, 4), dtype=np.float32), (4, 4), "out")
+    with pytest.raises(ValueError):
+        mf._host_out(np.empty((8, 4))[::2], (4, 4), "out")          # not contiguous
+    assert mf._host_out(None, (8, 4), "out").shape == (8, 4)
+    with pytest.raises(ValueError):
+        mf._host_square(np.eye(3), 4, "A")
+    with pytest.raises(ValueError):
+        mf.accel_inverse(np.eye(4), np.eye(3), 0.1, 2)             # E0 of the wrong size, no GPU call made
