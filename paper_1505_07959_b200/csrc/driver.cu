@@ -785,29 +785,18 @@ static int load_matrix(mfode_ctx* h, const double* src, bool host, size_t ld_src
   if (h->B) CUDA_TRY(h, launch_i_minus(h->B, h->A, h->n, h->ld, st));
   Rank& R = h->ranks[0];
   CUDA_TRY(h, launch_frob(h->A, nullptr, h->n, h->ld, R.partials, R.metric, 1, 0.0, nullptr, st));
-  CUDA_TRY(h, cudaMemcpyAsync(R.host_metric, R.metric, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // exact symmetry of A (the symmetric GEMM mode f3 relies on every iterate being a symmetric
+  // polynomial in A), checked on the device copy: A == A^T element by element (`!=`, so NaN fails)
+  int* asym_flag = reinterpret_cast<int*>(R.metric + 7);
+  CUDA_TRY(h, launch_check_symmetric(h->A, h->n, h->ld, asym_flag, st));
+  CUDA_TRY(h, cudaMemcpyAsync(R.host_metric, R.metric, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   h->normA = R.host_metric[1];
   h->has_result = false;
-  // exact symmetry of A (the symmetric GEMM mode f3 relies on every iterate being a symmetric
-  // polynomial in A); a device input is checked from a host copy
   {
-    std::vector<double> tmp;
-    const double* hA = src;
-    if (!host) {
-      tmp.resize((size_t)h->n * h->n);
-      CUDA_TRY(h, cudaMemcpy2D(tmp.data(), h->n * sizeof(double), src, ld_src * sizeof(double), h->n * sizeof(double),
-                               h->n, cudaMemcpyDeviceToHost));
-      hA = tmp.data();
-    }
-    const size_t lda = host ? ld_src : (size_t)h->n;
-    bool s = true;
-    for (int i = 0; i < h->n && s; ++i)
-      for (int j = i + 1; j < h->n; ++j)
-        if (hA[(size_t)i * lda + j] != hA[(size_t)j * lda + i]) {
-          s = false;
-          break;
-        }
+    int asym = 0;
+    memcpy(&asym, R.host_metric + 7, sizeof(int));
+    const bool s = (asym == 0);
     h->a_symmetric = s;
     if (!s) h->sym = false;
   }

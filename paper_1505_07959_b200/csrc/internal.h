@@ -36,6 +36,8 @@ extern bool g_pdl;   // programmatic dependent launch for the GEMM kernels (opti
 
 cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st);
 cudaError_t launch_i_minus(double* B, const double* A, int n, int ld, cudaStream_t st);
+// *flag = 1 iff A != A^T somewhere (exact, NaN counts as a mismatch); zeroes flag first
+cudaError_t launch_check_symmetric(const double* A, int n, int ld, int* flag, cudaStream_t st);
 // mode 0: out[0] = ||X-Y||/||X||; mode 1: out[0] = ||X-Y||, out[1] = ||X||.  partials: 2*296 doubles.
 cudaError_t launch_frob(const double* X, const double* Y, int n, int ld, double* partials, double* out, int mode,
                         double tol, int* stop_flag, cudaStream_t st);

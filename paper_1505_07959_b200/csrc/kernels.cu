@@ -362,6 +362,25 @@ __global__ void k_max_ptrs(PtrList l, double denom, double* out, double tol, int
   if (stop_flag) *stop_flag = (v <= tol) ? 1 : 0;
 }
 
+// flag = 1 if A != A^T anywhere (exact comparison, NaN counts as a mismatch); the caller zeroes flag.
+// One 32 x 32 tile pair (i <= j) per block, both tiles staged through shared memory (coalesced reads).
+__global__ void k_check_symmetric(const double* A, int n, int ld, int* flag) {
+  const int ti = blockIdx.y, tj = blockIdx.x;
+  if (ti > tj) return;
+  __shared__ double a[32][33], b[32][33];
+  const int r = threadIdx.y, cc = threadIdx.x;   // 32 x 8 threads
+  for (int rr = r; rr < 32; rr += 8) {
+    const int i1 = ti * 32 + rr, j1 = tj * 32 + cc;
+    a[rr][cc] = (i1 < n && j1 < n) ? A[(long long)i1 * ld + j1] : 0.0;
+    const int i2 = tj * 32 + rr, j2 = ti * 32 + cc;
+    b[rr][cc] = (i2 < n && j2 < n) ? A[(long long)i2 * ld + j2] : 0.0;
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int rr = r; rr < 32; rr += 8) bad |= (a[rr][cc] != b[cc][rr]);
+  if (__any_sync(0xffffffffu, bad) && cc == 0) *flag = 1;
+}
+
 // --------------------------------------------------------------------------------------------
 // host wrappers
 // --------------------------------------------------------------------------------------------
@@ -370,6 +389,15 @@ static int ew_grid(long long elems) {
   if (g > 148 * 16) g = 148 * 16;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+cudaError_t launch_check_symmetric(const double* A, int n, int ld, int* flag, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  const int t = (n + 31) / 32;
+  k_check_symmetric<<<dim3(t, t), dim3(32, 8), 0, st>>>(A, n, ld, flag);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st) {

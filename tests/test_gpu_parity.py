@@ -815,3 +815,26 @@ def test_fused_path_sequential_modified_and_ranks():
     Xe0 = np.empty((256, 256))
     se.result(Xe0)
     assert ie1["basis_size"] == ie0["basis_size"] and np.array_equal(Xe1, Xe0)
+
+
+def test_symmetry_check_on_device_is_exact():
+    """The symmetric mode (f3(i)) needs A == A^T bitwise; the check runs on the device copy of A (a tile-pair
+    kernel) for host and device inputs: one element off by one ulp, or a NaN, disables it."""
+    w = workloads.random_spd(100, 50)
+    A = w.A.copy()
+    s = mf.Solver(A, mf.FLOW_INVERSE, 1.0, 4, 1, 2)
+    s.set_option("symmetric", 1)
+    B = A.copy()
+    B[3, 97] = np.nextafter(B[3, 97], 2.0)
+    s.set_matrix(B)
+    with pytest.raises(mf.MfodeError):
+        s.set_option("symmetric", 1)
+    s.set_matrix(A)
+    s.set_option("symmetric", 1)
+    C = A.copy()
+    C[10, 10] = np.nan
+    sd = mf.Solver(torch.from_numpy(C).cuda(), mf.FLOW_INVERSE, 1.0, 4, 1, 2)
+    with pytest.raises(mf.MfodeError):
+        sd.set_option("symmetric", 1)
+    sd2 = mf.Solver(torch.from_numpy(A).cuda(), mf.FLOW_INVERSE, 1.0, 4, 1, 2)
+    sd2.set_option("symmetric", 1)
