@@ -161,6 +161,7 @@ struct mfode_ctx {
   double* X0dev = nullptr;   // MFODE_FLOW_AFFINE: U_0 (device copy; identity by default)
   bool phase_timing = true;  // option "phase_timing"
   int fused = -1;            // option "fused": K10 one-launch fine propagator (-1 auto, 0 off, 1 on)
+  int inject_nan = -1;       // option "inject_nan_slice": fault injection -- U^0_j := NaN after Step 0
   unsigned long long mat_gen = 0;   // content generation of A / B (emulated-GEMM encoding cache key)
   std::vector<mfode::Rank> ranks;
   // modified parareal (Algorithm 3): F-orthonormal basis Q of S^k, fine images F(Q), scratch
@@ -1054,6 +1055,15 @@ static int solve_impl(mfode_ctx* h, int K_max, double tol, int stop, mfode_solve
   }
   // ---- Step 0 ----
   for (auto& R : h->ranks) TRY(enqueue_step0(h, R));
+  // Fault injection (failure-detection test hook): overwrite U^0_j with NaNs once Step 0 has
+  // produced it (and G(U^0_j)), in the rank that propagates slice j; its fine work then waits for it.
+  if (h->inject_nan >= 1 && h->inject_nan < h->N)
+    for (auto& R : h->ranks)
+      if (h->inject_nan >= R.s0 && h->inject_nan < R.s1) {
+        CUDA_TRY(h, cudaMemsetAsync(slot(h, R.U[0], h->inject_nan - R.s0), 0xFF, state_elems(h) * sizeof(double),
+                                    R.coarse));
+        for (int j = 0; j < R.nloc; ++j) CUDA_TRY(h, cudaEventRecord(R.evC[j], R.coarse));
+      }
   double res0 = NAN;
   if (stop == MFODE_STOP_RESIDUAL && owns_last(h)) {
     int sp;
@@ -1680,6 +1690,11 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
   if (!strcmp(key, "fused")) {   // K10 one-launch fine propagator: -1 auto (64 < n <= 512), 0 off, 1 on
     if (value < -1 || value > 1) return fail(h, MFODE_EINVAL, "fused must be -1, 0 or 1");
     h->fused = (int)value;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "inject_nan_slice")) {   // test hook: 1..N-1 poisons U^0_j after Step 0; <= 0 disables
+    if (value >= h->N) return fail(h, MFODE_EINVAL, "inject_nan_slice must be < N");
+    h->inject_nan = value >= 1 ? (int)value : -1;
     return MFODE_OK;
   }
   if (!strcmp(key, "phase_timing")) {   // per-phase CUDA-event spans (mfode_solve_info ms_coarse ...)

@@ -838,3 +838,20 @@ def test_symmetry_check_on_device_is_exact():
         sd.set_option("symmetric", 1)
     sd2 = mf.Solver(torch.from_numpy(A).cuda(), mf.FLOW_INVERSE, 1.0, 4, 1, 2)
     sd2.set_option("symmetric", 1)
+
+
+@pytest.mark.parametrize("world,j", [(1, 3), (2, 5), (3, 2)])
+def test_fault_injection_names_first_bad_slice(world, j):
+    """Failure detection: the test hook poisons U^0_j after Step 0.  F(U^0_j) is then
+    NaN, so the first correction sweep makes U^1_{j+1} non-finite while U^1_j (from slice j-1) stays
+    finite: the solve must stop with ENONFINITE at k = 1 and name slice j + 1, on any rank layout."""
+    w = workloads.random_spd(64, 60)
+    N = 8
+    s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 4, world=world)
+    s.set_option("inject_nan_slice", j)
+    with pytest.raises(mf.MfodeError) as e:
+        s.solve(4, 1e-12, mf.STOP_DELTA)
+    assert e.value.status == mf.ENONFINITE
+    assert e.value.info["k_done"] == 1 and e.value.info["bad_slice"] == j + 1
+    s.set_option("inject_nan_slice", 0)
+    assert s.solve(4, 1e-12, mf.STOP_DELTA)["k_done"] >= 1      # the handle stays usable
