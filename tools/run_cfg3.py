@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--skip-full", action="store_true")
     ap.add_argument("--skip-sym", action="store_true")
     ap.add_argument("--modes", nargs="*", default=None,
-                    help="subset of: full symmetric emulated emulated_symmetric (default: full symmetric)")
+                    help="subset of: full symmetric emulated emulated_symmetric seqfine (default: full symmetric)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     t0 = time.time()
@@ -41,6 +41,14 @@ def main():
     names = args.modes
     if names is None:
         names = [m for m, skip in (("full", args.skip_full), ("symmetric", args.skip_sym)) if not skip]
+    if "seqfine" in names:   # the K = N reference: 64 slices x 128 RK4 steps, sequential
+        names = [m for m in names if m != "seqfine"]
+        q = s.sequential_fine()
+        X = s.result()
+        rel = float(np.linalg.norm(X - ref) / np.linalg.norm(ref))
+        print(json.dumps({"stage": "sequential_fine", "ms": q["ms_total"],
+                          "fine_tflops": q["fine_flops"] / (q["ms_total"] * 1e-3) / 1e12,
+                          "rel_frob_vs_spectral_parareal": rel, "launches": q["gpu_launches"]}), flush=True)
     modes = [(m, *table[m]) for m in names]
     for name, sym, emu in modes:
         s.set_option("symmetric", sym)
