@@ -194,7 +194,9 @@ MFODE_API int mfode_get_slice(mfode_ctx *h, int n_index, double *U);
  * moduli, see mfode_dgemm_emulated; EINVAL if n leaves fewer than 8 bits per operand).  Process-wide
  * keys (they affect every handle of the process): "pdl" (1 = programmatic dependent launch of
  * consecutive GEMMs, default; 0 = plain stream order), "oz_pair" (1 = CTA-pair int8 GEMM kernel,
- * default; 0 = single-CTA kernel; results are bitwise identical).  Per handle also: "fused" (-1 = auto: the one-launch fine propagator K10 for 64 < n <= 512, 0 = off,
+ * default; 0 = single-CTA kernel; results are bitwise identical), "cta_share_us" (bounded persistence of the
+ * DMMA GEMM's CTAs, microseconds of tiles each; default 2000, 500 once a multi-rank NCCL communicator is
+ * created; results are bitwise identical).  Per handle also: "fused" (-1 = auto: the one-launch fine propagator K10 for 64 < n <= 512, 0 = off,
  * 1 = on where eligible; bitwise identical), "phase_timing" (1 = per-phase CUDA-event spans in
  * mfode_solve_info, default; 0 = off) and the failure-detection test hook "inject_nan_slice" (j in 1..N-1:
  * mfode_parareal_solve overwrites U^0_j with NaN after Step 0, so the solve must end in MFODE_ENONFINITE

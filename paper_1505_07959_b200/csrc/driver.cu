@@ -637,7 +637,14 @@ static int enqueue_correction(mfode_ctx* h, Rank& R, int k) {
   NvtxRange nv("mfode:correction");
   const int cur = k % 2, nxt = (k + 1) % 2;
   const int j0 = std::max(0, k - R.s0);
-  if (k < R.s0) TRY(recv_boundary(h, R, nxt));
+  if (k < R.s0) {
+    // NCCL: the upstream rank sends its boundary only after ITS correction sweep, i.e. about when this
+    // rank's fine sweep ends; posting the receive earlier would park NCCL's kernel on SMs for the whole
+    // fine sweep (every persistent fine launch would then run with a tail).  Waiting for this rank's
+    // last fine chunk first costs nothing on the critical path.
+    if (h->nccl_mode && R.nloc > 0) CUDA_TRY(h, cudaStreamWaitEvent(R.coarse, R.evF[R.chunk_of[R.nloc - 1]], 0));
+    TRY(recv_boundary(h, R, nxt));
+  }
   if (h->small) {
     // the single-CTA sweep needs every F(U^k_n), n >= j0, before it starts
     for (int j = j0; j < R.nloc; ++j)
@@ -857,6 +864,7 @@ static int create_impl(mfode_ctx** out, const double* A, bool host, int64_t n, i
       r = nccl().commInitRank(&h->comm, world, uid, dist->rank);
     }
     if (r != ncclSuccess) return set_global_err(MFODE_ENCCL, "ncclCommInitRank failed: %d", (int)r);
+    if (world > 1 && g_cta_share_s > 0.5e-3) g_cta_share_s = 0.5e-3;   // see internal.h
   }
   // fine batch capacity: enough batched tiles to fill the chip, bounded by the slice count
   {
@@ -1733,6 +1741,11 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
   }
   if (!strcmp(key, "pdl")) {   // process-wide: programmatic dependent launch of the GEMMs
     g_pdl = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "cta_share_us")) {   // process-wide: DMMA GEMM bounded persistence (us of tiles per CTA)
+    if (value < 10 || value > 1000000) return fail(h, MFODE_EINVAL, "cta_share_us must be in [10, 1e6]");
+    g_cta_share_s = value * 1e-6;
     return MFODE_OK;
   }
   if (!strcmp(key, "small")) {

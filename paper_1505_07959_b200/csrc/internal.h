@@ -33,6 +33,10 @@ inline int cur_device() {
   return dev;
 }
 extern bool g_pdl;   // programmatic dependent launch for the GEMM kernels (option "pdl")
+// Bounded persistence of the DMMA GEMM: seconds of tiles per CTA (option "cta_share_us"; 2 ms, or 0.5 ms
+// once a multi-rank NCCL communicator exists, whose parked kernels may hold SMs: with static tile
+// ownership every SM held by another kernel delays one CTA share to the end of each launch).
+extern double g_cta_share_s;
 
 cudaError_t launch_identity(double* X, int n, int ld, int count, long long zstride, cudaStream_t st);
 cudaError_t launch_i_minus(double* B, const double* A, int n, int ld, cudaStream_t st);

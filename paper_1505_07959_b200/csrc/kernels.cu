@@ -25,6 +25,7 @@ namespace mfode {
 
 std::atomic<long long> g_launches{0};
 bool g_pdl = true;
+double g_cta_share_s = 2e-3;
 
 // --------------------------------------------------------------------------------------------
 // Element-wise kernels (HBM-bound; 16-byte vector accesses; padding columns kept at zero)
@@ -612,7 +613,7 @@ static cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, cons
   // that pinned every SM for a whole (batched, ~100 ms) launch would starve the high-priority coarse
   // stream (the sequential critical path); retiring CTAs every ~2 ms lets its CTAs in.
   const double tile_s = 2.0 * BM * BN * (double)p.n / (37e12 / (num_sms() * occ));
-  const long long max_tiles_per_cta = std::max<long long>(1, (long long)(2e-3 / tile_s));
+  const long long max_tiles_per_cta = std::max<long long>(1, (long long)(g_cta_share_s / tile_s));
   // The grid is a whole number of waves (a multiple of the resident-CTA slots), so the static
   // round-robin gives every CTA floor/ceil(tiles / grid) tiles and no wave is left half empty.
   // (A per-stream atomic tile ticket was built in round 2 and measured 1.3 % slower on this kernel,
