@@ -855,3 +855,21 @@ def test_fault_injection_names_first_bad_slice(world, j):
     assert e.value.info["k_done"] == 1 and e.value.info["bad_slice"] == j + 1
     s.set_option("inject_nan_slice", 0)
     assert s.solve(4, 1e-12, mf.STOP_DELTA)["k_done"] >= 1      # the handle stays usable
+
+
+def test_cta_share_bitwise_invariant():
+    """Bounded persistence (process-wide option cta_share_us: how much of a launch each persistent CTA
+    owns) changes the grid and tile-to-CTA assignment only, never an element's k order: bitwise equal."""
+    w = workloads.random_spd(700, 61)
+    outs = []
+    try:
+        for share in (2000, 60):
+            s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, 6, 1, 4)
+            s.set_option("cta_share_us", share)
+            s.solve(3)
+            outs.append(s.result())
+            s.close()
+    finally:
+        s = mf.Solver(np.eye(4), mf.FLOW_INVERSE, 1.0, 2, 1, 1)
+        s.set_option("cta_share_us", 2000)
+    assert np.array_equal(outs[0], outs[1])
