@@ -78,7 +78,11 @@ __device__ __forceinline__ PhaseInfo phase_info(int g, int gps) {
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
+// 168 registers per thread at launch: three warps share one SM sub-partition (16K registers) in both
+// configurations -- 12 warps of the 8-consumer-warp CTA, 2 x 5 warps of two resident 4-warp CTAs --
+// so a 169th register halves the 4-warp configuration's occupancy (seen at 173 registers: 2 -> 1
+// CTA per SM, 29.2 -> 20.7 TF/s at n = 256 with 32 slices).
+__global__ void __maxnreg__(168)
     fine_fused_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>;
   constexpr int kQ = 8;   // tile-info ring (the producer runs at most STAGES tiles ahead)
@@ -234,6 +238,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
   }
 
   // ===================== consumers: DMMA main loop + fused epilogue =====================
+  // Stage release after the stage's DMMAs are issued, without the proxy fence the launch-per-GEMM
+  // path needs for its earlier release (same-box A/B: n = 256 / 16 slices 27.07 -> 27.60 TF/s, cfg[1]
+  // 108.1 -> 106.0 ms; 4-warp configuration +4-5 % at n = 256..512, profiles/ab_k10_r02.jsonl).
+  constexpr bool kLateRelease = true;
   const int wm = warp / WARPS_N;
   const int wn = warp % WARPS_N;
   const int g8 = lane >> 2;
@@ -287,9 +295,11 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
           }
         }
         if (kb == 1) {
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
+          if constexpr (!kLateRelease) {
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+          }
           const int ns = (stage + 1 == STAGES) ? 0 : stage + 1;
           ready = (kt + 1 < KT) && mbar_test_wait(&full[ns], ns == 0 ? (phase ^ 1) : phase);
         }
@@ -304,6 +314,13 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
               dmma(acc[mt][2 * ng + 1][0], acc[mt][2 * ng + 1][1], a, bf[ng][s].y);
             }
           }
+      }
+      if constexpr (kLateRelease) {
+        // every fragment read from the stage has been consumed by an issued DMMA (a DMMA issues
+        // only once its source registers are written), so this warp's shared-memory reads of the
+        // stage are complete and the TMA refill cannot race them: no proxy fence needed
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
       }
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }

@@ -116,9 +116,10 @@ struct FusedLaunch {
   unsigned* sched;
 };
 cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st);
-// scheduler words of a fused launch: the ticket + per slice rowK[tm], colK[tn], colW[tn] (64 x 64 tiles)
+// scheduler words of a fused launch: the ticket + per slice rowK[tm], colK[tn], colW[tn] (tiles of at
+// least 32 columns / 64 rows; sized for 32 x 32 so every tile configuration fits)
 inline size_t fused_sched_words(int Z, int n) {
-  const size_t t = (size_t)(n + 63) / 64;
+  const size_t t = (size_t)(n + 31) / 32;
   return 1 + (size_t)Z * 3 * t;
 }
 

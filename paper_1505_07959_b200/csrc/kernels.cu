@@ -724,9 +724,8 @@ static cudaError_t launch_fused_cfg(const FusedMaps& maps, const FusedParams& p,
   return e;
 }
 
-cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st) {
-  // one tile config (64 x 64, 4 consumer warps, two or more CTAs per SM): the path serves n <= 512
-  constexpr int BM = 64, BN = 64;
+template <int BM, int BN, int WM_, int WN_, int ST>
+static cudaError_t launch_fine_fused_tiles(const FusedLaunch& L, cudaStream_t st) {
   const int n = L.n, ld = L.ld;
   FusedMaps maps;
   const int rows_a = BM;
@@ -768,12 +767,19 @@ cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st) {
   p.total = (long long)L.mF * 4 * p.gps * L.Z * p.T_tiles;
   cudaError_t e = cudaMemsetAsync(L.sched, 0, sizeof(unsigned) * fused_sched_words(L.Z, n), st);
   if (e != cudaSuccess) return e;
-  // Few tiles per phase (Z * T <= 2 per SM): one 8-consumer-warp CTA per SM finishes each tile twice
-  // as fast, shortening every slice's phase chain (the critical path); with more tiles, two 4-warp
-  // CTAs per SM overlap one CTA's dependency waits and epilogue with the other's main loop
-  // (measured, profiles/fused_r02.md).
-  if ((long long)L.Z * p.T_tiles <= 2LL * num_sms()) return launch_fused_cfg<BM, BN, 2, 4, 4>(maps, p, st);
-  return launch_fused_cfg<BM, BN, 2, 2, 4>(maps, p, st);
+  return launch_fused_cfg<BM, BN, WM_, WN_, ST>(maps, p, st);
+}
+
+// Tile configuration by parallelism, always two 4-consumer-warp CTAs per SM (one CTA's dependency
+// waits and epilogue overlap the other's main loop).  Few tiles per phase (Z * T64 <= 2 per SM):
+// 64 x 32 tiles, so each tile takes half as long and every slice's phase chain -- the critical path
+// -- is shorter; more tiles: 64 x 64 (twice the operand reuse).  Same-box A/B (profiles/
+// ab_k10_r02.jsonl): n = 256 with 16 slices 27.1 (one 8-warp CTA per SM, 64 x 64) -> 28.2 TF/s,
+// cfg[1] 108.1 -> 103.1 ms; 64 x 32 everywhere loses 7-10 % at 32+ slices.  Serves n <= 512.
+cudaError_t launch_fine_fused(const FusedLaunch& L, cudaStream_t st) {
+  const long long tiles64 = (long long)L.Z * ((L.n + 63) / 64) * ((L.n + 63) / 64);
+  if (tiles64 <= 2LL * num_sms()) return launch_fine_fused_tiles<64, 32, 2, 2, 4>(L, st);
+  return launch_fine_fused_tiles<64, 64, 2, 2, 4>(L, st);
 }
 
 // --------------------------------------------------------------------------------------------

@@ -790,7 +790,7 @@ def test_fused_path_sequential_modified_and_ranks():
     """K10 under every caller: sequential fine (K = N bitwise, P5), logical ranks (P9), the modified
     parareal's batched fine images, and repeated tolerance solves (strictly phased: see solve_impl).  N = 24
     slices of n = 256 (384 tiles per phase) run the two-CTAs-per-SM configuration, the sequential
-    runs (one slice) the 8-warp one."""
+    runs (one slice) the 64 x 32 one."""
     w = workloads.random_spd(256, 41)
     N = 24
     s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, N, 1, 8)
