@@ -238,10 +238,6 @@ __global__ void __maxnreg__(168)
   }
 
   // ===================== consumers: DMMA main loop + fused epilogue =====================
-  // Stage release after the stage's DMMAs are issued, without the proxy fence the launch-per-GEMM
-  // path needs for its earlier release (same-box A/B: n = 256 / 16 slices 27.07 -> 27.60 TF/s, cfg[1]
-  // 108.1 -> 106.0 ms; 4-warp configuration +4-5 % at n = 256..512, profiles/ab_k10_r02.jsonl).
-  constexpr bool kLateRelease = true;
   const int wm = warp / WARPS_N;
   const int wn = warp % WARPS_N;
   const int g8 = lane >> 2;
@@ -295,11 +291,6 @@ __global__ void __maxnreg__(168)
           }
         }
         if (kb == 1) {
-          if constexpr (!kLateRelease) {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-          }
           const int ns = (stage + 1 == STAGES) ? 0 : stage + 1;
           ready = (kt + 1 < KT) && mbar_test_wait(&full[ns], ns == 0 ? (phase ^ 1) : phase);
         }
@@ -315,13 +306,11 @@ __global__ void __maxnreg__(168)
             }
           }
       }
-      if constexpr (kLateRelease) {
-        // every fragment read from the stage has been consumed by an issued DMMA (a DMMA issues
-        // only once its source registers are written), so this warp's shared-memory reads of the
-        // stage are complete and the TMA refill cannot race them: no proxy fence needed
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-      }
+      // stage release after the consuming DMMAs are issued (no proxy fence), as in gemm.cuh (same-box
+      // A/B here: n = 256 / 16 slices 27.07 -> 27.60 TF/s, 4-warp configuration +4-5 %,
+      // profiles/ab_k10_r02.jsonl)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
     ++seq;

@@ -278,15 +278,8 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
           }
         }
         if (kb == 1) {
-          // Every shared-memory read of this stage is issued: release it to the producer now,
-          // and probe the next stage's full barrier so the probe's latency hides behind this
-          // k-step's DMMAs instead of stalling the next one.  The producer refills the stage
-          // with TMA (async proxy), so the generic-proxy reads must be ordered before it by a
-          // proxy fence: without it a still-pending ld.shared could observe the refill (seen as
-          // rare wrong 32 x 16 warp sub-tiles when the producer waits at the stage).
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
+          // Probe the next stage's full barrier now, so the probe's latency hides behind this
+          // k-step's DMMAs instead of stalling the next one.
           const int ns = (stage + 1 == STAGES) ? 0 : stage + 1;
           ready = (kt + 1 < KT) && mbar_test_wait(&full[ns], ns == 0 ? (phase ^ 1) : phase);
         }
@@ -302,6 +295,14 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
             }
           }
       }
+      // Release the stage to the producer once the DMMAs that consume its fragments are issued: a
+      // DMMA issues only after its source registers are written, so every shared-memory read of the
+      // stage by this warp has completed and the TMA (async-proxy) refill cannot race it.  (Releasing
+      // right after the last ld.shared, with reads still in flight, needs a proxy fence -- without
+      // one, rare wrong 32 x 16 warp sub-tiles were seen -- and the fence's wait costs more: same-box
+      // A/B 34.63 -> 34.72 TF/s per RK stage at n = 4096, profiles/ab_gemm_late_release_r02.jsonl.)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
 
