@@ -242,6 +242,7 @@ def main():
                     help="timed solves of the f3(ii) int8-tensor-core emulated variant (0: skip)")
     ap.add_argument("--emu-moduli", type=int, default=16)
     ap.add_argument("--no-seqfine", action="store_true", help="skip timing mfode_sequential_fine (the K = N reference)")
+    ap.add_argument("--no-cfg2", action="store_true", help="secondary lines: skip the ~70 s cfg[2] solve")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
                     help="skip the cfg[0] / cfg[1] iteration-dynamics lines reported beside the headline")
     ap.add_argument("--plumbing-test", action="store_true",
@@ -426,25 +427,32 @@ def main():
     emu_sym = (variant({"emulation": args.emu_moduli, "symmetric": 1}, args.emu_steps)
                if args.emu_steps > 0 else None)
 
-    # The headline config converges at k = 1 (one fine sweep); the smaller BASELINE configs exercise
-    # the iteration (k_done 4 and 6) on the other fine-propagator kernels (K6 at n = 32, K10 at
-    # n = 256).  Reported beside the headline, one GPU (rank 0 alone), not folded into `value`.
+    # The headline config converges at k = 1 (one fine sweep); the other BASELINE configs exercise
+    # the iteration (k_done 4, 6 and 8) on the other fine-propagator kernels (K6 at n = 32, K10 at
+    # n = 256, the batched DMMA GEMM with speculative next-sweep overlap at n = 1024).  Reported
+    # beside the headline, one GPU (rank 0 alone), not folded into `value`.  cfg[2] is one ~64 s
+    # solve (warmed by a coarse-only K = 0 solve), so it is timed once; --no-cfg2 skips it.
     secondary = None
     if world == 1 and args.secondary:
         secondary = []
-        for c in (0, 1):
+        for c in ((0, 1) if args.no_cfg2 else (0, 1, 2)):
             wc = workloads.config(c, with_eig=False)
             sc = mf.Solver(wc.A, wc.flow, wc.T, wc.N, wc.m_G, wc.m_F)
-            sc.solve(wc.K_max, wc.tol, wc.stop)   # warm-up
-            ic = [sc.solve(wc.K_max, wc.tol, wc.stop) for _ in range(3)]
+            reps = 3 if c < 2 else 1
+            sc.solve(wc.K_max if c < 2 else 0, wc.tol, wc.stop)   # warm-up
+            ic = [sc.solve(wc.K_max, wc.tol, wc.stop) for _ in range(reps)]
             ms = float(np.mean([i["ms_total"] for i in ic]))
             sq = sc.sequential_fine()
             kf = ic[-1]
+            kname = ("K6 fine_smem_kernel" if wc.n <= 64 else
+                     "K10 fine_fused_kernel" if wc.n <= 512 else "dgemm_tma_kernel (batched, fused RK epilogue)")
             secondary.append({
-                "workload": wc.name, "n": wc.n, "N_slices": wc.N, "k_done": kf["k_done"],
+                "workload": wc.name, "n": wc.n, "N_slices": wc.N, "k_done": kf["k_done"], "timed_solves": reps,
+                "deltas": kf.get("deltas"),
                 "time_to_tol_ms": ms, "fine_tflops_whole_solve": kf["fine_flops"] / (ms * 1e-3) / 1e12,
                 "fine_kernel_tflops": kf["fine_kernel_flops"] / (kf["fine_kernel_ms"] * 1e-3) / 1e12,
-                "fine_kernel": "K6 fine_smem_kernel" if wc.n <= 64 else "K10 fine_fused_kernel",
+                "fine_kernel": kname,
+                "phases_ms": {k: kf.get(k) for k in ("ms_coarse", "ms_fine", "ms_correct", "ms_comm")},
                 "gpu_launches_per_solve": kf["gpu_launches"], "sequential_fine_ms": sq["ms_total"],
                 "speedup_vs_sequential_fine": sq["ms_total"] / ms})
             sc.close()
