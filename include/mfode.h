@@ -188,7 +188,10 @@ MFODE_API int mfode_get_slice(mfode_ctx *h, int n_index, double *U);
 /* Tuning knobs (all optional).  key: "fine_batch" (max slices per batched fine launch; 0 = auto),
  * "overlap" (1 = speculative next-iteration fine work overlapped with the correction sweep,
  * 0 = strictly phased), "tile" (0 = auto, 1 = 128x128, 2 = 64x64, 3 = 32x64 GEMM tiles), "small" (1 = K6
- * shared-memory persistent kernels, default for n <= 64; 0 = one launch per GEMM), "symmetric" (1 = f3(i)
+ * shared-memory persistent kernels, default for n <= 64; 0 = one launch per GEMM), "small_cluster" (K6 CTAs
+ * per slice: 1 = one CTA, 2 / 4 (/ 8 for 32 < n <= 64) = a thread-block cluster splitting the columns,
+ * new stage values exchanged through distributed shared memory; -1 = auto by n and flow; bitwise identical),
+ * "symmetric" (1 = f3(i)
  * half-flop symmetric GEMMs, needs A == A^T bitwise), "emulation" (f3(ii): 0 = FP64 DMMA GEMMs;
  * 8..16 = every GEMM except the residual's emulated on the int8 tensor cores with that many CRT
  * moduli, see mfode_dgemm_emulated; EINVAL if n leaves fewer than 8 bits per operand).  Process-wide

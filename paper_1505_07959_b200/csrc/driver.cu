@@ -161,6 +161,7 @@ struct mfode_ctx {
   double* X0dev = nullptr;   // MFODE_FLOW_AFFINE: U_0 (device copy; identity by default)
   bool phase_timing = true;  // option "phase_timing"
   int fused = -1;            // option "fused": K10 one-launch fine propagator (-1 auto, 0 off, 1 on)
+  int small_cs = -1;         // option "small_cluster": K6 CTAs per slice (-1 auto, 1, 2, 4, 8)
   int inject_nan = -1;       // option "inject_nan_slice": fault injection -- U^0_j := NaN after Step 0
   unsigned long long mat_gen = 0;   // content generation of A / B (emulated-GEMM encoding cache key)
   std::vector<mfode::Rank> ranks;
@@ -413,6 +414,17 @@ static bool use_fused(const mfode_ctx* h) {
   return eligible && h->n > kSmallMaxN;
 }
 
+// K6 CTAs per slice unless the option fixes it (bitwise identical).  Measured on B200 (tools/k6c_probe.cu,
+// profiles/k6c_probe_sizes_r02.log, us per RK4 step for 8 slices, CTAs per slice 1 / 2 / 4 / 8):
+//   n <= 32: inverse 3.00 / 2.37 / 3.58, sqrt 1.95 / 2.24 / 3.62, exp 1.57 / 1.31 / 1.19
+//   n <= 64: inverse 18.9 / 11.7 / 9.0 / 14.2, sqrt 10.3 / 8.3 / 7.8 / 13.9, exp 9.8 / 5.3 / 3.0 / 1.95
+// (the sqrt flow's exchange sits on its critical path: no column-local GEMM hides it)
+static int small_cluster(const mfode_ctx* h) {
+  if (h->small_cs > 0) return h->small_cs;
+  if (h->n <= 32) return h->flow == MFODE_FLOW_INVERSE ? 2 : (h->flow == MFODE_FLOW_EXP ? 4 : 1);
+  return h->flow == MFODE_FLOW_EXP ? 8 : 4;
+}
+
 static int fine_prop(mfode_ctx* h, Rank& R, const double* in, int in_count, double* out, int out_count, int ja,
                      int jb, const int* stop_flag) {
   const int Z = jb - ja;
@@ -447,7 +459,7 @@ static int fine_prop(mfode_ctx* h, Rank& R, const double* in, int in_count, doub
   if (h->small) {
     const double* M = (h->flow == MFODE_FLOW_INVERSE) ? h->B : h->A;
     CUDA_TRY(h, launch_fine_small(h->flow, h->n, h->ld, M, in + (size_t)ja * state_elems(h),
-                                  slot(h, out, ja), me, Z, h->mF, hF, stop_flag, R.fine));
+                                  slot(h, out, ja), me, Z, h->mF, hF, stop_flag, small_cluster(h), R.fine));
     return MFODE_OK;
   }
   // batch index = sub-matrix index (ms per state)
@@ -1752,6 +1764,12 @@ int mfode_set_option(mfode_ctx* h, const char* key, int64_t value) {
     if (value && (h->n > kSmallMaxN || h->ms != 1 || h->flow == MFODE_FLOW_AFFINE))
       return fail(h, MFODE_EINVAL, "small kernels need n <= %d, a one-matrix state and no source", kSmallMaxN);
     h->small = value != 0;
+    return MFODE_OK;
+  }
+  if (!strcmp(key, "small_cluster")) {
+    if (value != -1 && value != 1 && value != 2 && value != 4 && !(value == 8 && h->n > 32))
+      return fail(h, MFODE_EINVAL, "small_cluster must be -1 (auto), 1, 2, 4 (or 8 for 32 < n <= 64)");
+    h->small_cs = (int)value;
     return MFODE_OK;
   }
   if (!strcmp(key, "tile")) {

@@ -123,9 +123,10 @@ inline size_t fused_sched_words(int Z, int n) {
   return 1 + (size_t)Z * 3 * t;
 }
 
-// K6: all m_F RK4 steps of Z slices (one CTA each) in shared memory; M = B (inverse) or A (sqrt)
+// K6: all m_F RK4 steps of Z slices in shared memory; M = B (inverse) or A (sqrt).  cs = 1: one CTA
+// per slice; cs = 2, 4 (n <= 32) or 2, 4, 8 (n <= 64): one cluster of cs CTAs per slice (K6c)
 cudaError_t launch_fine_small(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
-                              long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st);
+                              long long mstride, int Z, int mF, double h, const int* flag, int cs, cudaStream_t st);
 // K6: the rank's sequential coarse sweep (Step 0 if correct == 0, else the correction) in one CTA
 cudaError_t launch_coarse_small(int flow, int n, int ld, const double* M, const double* Vin, double* U, double* Gold,
                                 const double* Fk, long long mstride, int j0, int nloc, int mG, double h, int correct,

@@ -813,9 +813,44 @@ static cudaError_t coarse_small_np(int flow, int n, int ld, const double* M, con
   return cudaGetLastError();
 }
 
+// K6c: Z clusters of CS CTAs, one slice per cluster (small.cuh fine_cluster_kernel)
+template <int NP, int CS>
+static cudaError_t fine_cluster_np(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
+                                   long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st) {
+  using C = ClusterCfg<NP, CS>;
+  const size_t smem = 5 * C::MAT * sizeof(double);   // M, X, Y_a, Y_b, W (S in registers)
+  auto kern = fine_cluster_kernel<NP, CS>;
+  static std::once_flag once[kMaxDevices];
+  std::call_once(once[cur_device()], [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(Z * CS));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, flow, n, ld, M, Uin, Fout, mstride, mF, h, flag);
+  ++g_launches;
+  return e;
+}
+
 cudaError_t launch_fine_small(int flow, int n, int ld, const double* M, const double* Uin, double* Fout,
-                              long long mstride, int Z, int mF, double h, const int* flag, cudaStream_t st) {
-  if (n <= 32) return fine_small_np<32>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+                              long long mstride, int Z, int mF, double h, const int* flag, int cs, cudaStream_t st) {
+  if (n <= 32) {
+    if (cs == 2) return fine_cluster_np<32, 2>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+    if (cs == 4) return fine_cluster_np<32, 4>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+    return fine_small_np<32>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+  }
+  if (cs == 2) return fine_cluster_np<64, 2>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+  if (cs == 4) return fine_cluster_np<64, 4>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
+  if (cs == 8) return fine_cluster_np<64, 8>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
   return fine_small_np<64>(flow, n, ld, M, Uin, Fout, mstride, Z, mF, h, flag, st);
 }
 

@@ -280,6 +280,314 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------------
+// K6c: one slice's fine propagation spread over a cluster of CS CTAs (one per SM), column-split.
+//
+// CTA q of the cluster owns a set of output columns (NP/CS of them) of every GEMM and of the RK state.
+// A column split keeps most of each stage local: W[:, own] = B Y[:, own] needs only the own columns
+// of Y, the stage combination and the RK state (X, S) are element-wise, and only the A-role operand of
+// K = Y W (inverse flow) or Y Y (sqrt flow) needs every column of Y.  So each stage exchanges its new
+// Y once: every thread pushes its own elements of Y_out into the other CTAs' copies with
+// st.async ... mbarrier::complete_tx (DSMEM stores that count bytes on the receiver's mbarrier), and
+// the receiver waits for (CS-1) x NP x NP/CS x 8 bytes just before the GEMM that needs them -- for the
+// inverse flow after W = B Y[:, own], so the exchange latency hides under that GEMM.  The exp flow
+// (K = A Y[:, own]) is column-local and exchanges nothing.
+//
+// Per output element the DMMA sequence (k = 8 kb + 2 c + s, kb-major) is the one of smem_gemm and
+// gemm.cuh, so results are bitwise identical to fine_smem_kernel and to the launch-per-GEMM path.
+//
+// Exchange t (the Y_out of global stage t = 4 step + s - 1) lands on xbar[t & 1].  A CTA can run at
+// most one exchange ahead of any other (its stage t+1 GEMM waits for exchange t from everyone), so two
+// alternating barriers keep every phase unambiguous; every write into a peer's buffer Y_out(t) happens
+// after the peer's threads all finished reading it as Y_in(t-1) (the peer's exchange t-1 bytes, sent by
+// each thread after its own stage t-1 GEMMs, had to arrive first).
+// ------------------------------------------------------------------------------------------------
+template <int NP, int CS>
+struct ClusterCfg {
+  static constexpr int MAT = NP * NP;
+  static constexpr int NPC = NP / CS;                   // columns owned by one CTA
+  static constexpr bool PSPLIT = (NPC == 8);            // a CTA owns one parity n-tile of a 16-column group
+  static constexpr int GC = PSPLIT ? 1 : NPC / 16;      // 16-column groups per CTA
+  static constexpr int NPAR = PSPLIT ? 1 : 2;           // n-tiles per group held by a thread
+  static constexpr int MT = NP / 8;                     // m-tiles
+  static constexpr int UNITS = MT * GC;
+  static constexpr int WARPS = UNITS < 8 ? UNITS : 8;
+  static constexpr int WARPS_G = GC;
+  static constexpr int WARPS_M = WARPS / WARPS_G;
+  static constexpr int WT_M = MT / WARPS_M;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr uint32_t XBYTES = (uint32_t)(CS - 1) * NP * NPC * 8;   // received per exchange
+  static_assert(NPC >= 8 && NP % CS == 0 && WARPS % WARPS_G == 0 && MT % WARPS_M == 0, "cluster split");
+};
+
+template <int NP, int CS>
+struct ClAcc {
+  double v[ClusterCfg<NP, CS>::WT_M][ClusterCfg<NP, CS>::NPAR][2];   // [m-tile][n-tile][e]
+};
+
+template <int NP, int CS>
+struct ClAFrag {
+  double2 f[ClusterCfg<NP, CS>::WT_M][NP / 8];
+};
+
+// owner coordinates of this thread: first row of m-tile mi is 8 (wm WT_M + mi); the thread's columns
+// are 16 grp + 4 c + 2 e + par(p)
+template <int NP, int CS>
+struct ClPos {
+  int wm, grp, par0, g, c;
+  __device__ __forceinline__ ClPos(uint32_t q) {
+    using C = ClusterCfg<NP, CS>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    wm = warp / C::WARPS_G;
+    const int wg = warp % C::WARPS_G;
+    grp = C::PSPLIT ? (int)(q >> 1) : (int)q * C::GC + wg;
+    par0 = C::PSPLIT ? (int)(q & 1) : 0;
+    g = lane >> 2;
+    c = lane & 3;
+  }
+  __device__ __forceinline__ int row(int mi) const { return (wm * ClusterCfg<NP, CS>::WT_M + mi) * 8 + g; }
+  __device__ __forceinline__ int col(int p, int e) const { return 16 * grp + 4 * c + 2 * e + par0 + p; }
+};
+
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(cta));
+  return r;
+}
+// DSMEM store into a peer CTA counted as transaction bytes on the peer's mbarrier (both addresses
+// already mapped to the peer)
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_1(uint32_t raddr, double a, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(raddr), "d"(a),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ int ld_cluster_s32(uint32_t raddr) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];\n" : "=r"(v) : "r"(raddr) : "memory");
+  return v;
+}
+
+// acc = P[own rows, :] * Q[:, own columns]; P from smem or (REGA) register fragments
+template <int NP, int CS, bool REGA>
+__device__ __forceinline__ void cl_gemm(const ClPos<NP, CS>& o, const double* __restrict__ P,
+                                        const double* __restrict__ Q, ClAcc<NP, CS>& acc,
+                                        const ClAFrag<NP, CS>* fr) {
+  using C = ClusterCfg<NP, CS>;
+  const uint32_t sP = smem_u32(P), sQ = smem_u32(Q);
+#pragma unroll
+  for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+    for (int p = 0; p < C::NPAR; ++p) acc.v[mi][p][0] = acc.v[mi][p][1] = 0.0;
+#pragma unroll
+  for (int kb = 0; kb < NP / 8; ++kb) {
+    double2 af[C::WT_M];
+#pragma unroll
+    for (int mi = 0; mi < C::WT_M; ++mi) {
+      if constexpr (REGA) {
+        af[mi] = fr->f[mi][kb];
+      } else {
+        af[mi] = lds128(sP + 8u * (uint32_t)sidx<NP>(o.row(mi), 8 * kb + 2 * o.c));
+      }
+    }
+    double bf[2][C::NPAR];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int k = 8 * kb + 2 * o.c + s;
+      if constexpr (C::PSPLIT) {
+        bf[s][0] = lds64(sQ + 8u * (uint32_t)sidx<NP>(k, 16 * o.grp + 2 * o.g + o.par0));
+      } else {
+        const double2 b = lds128(sQ + 8u * (uint32_t)sidx<NP>(k, 16 * o.grp + 2 * o.g));
+        bf[s][0] = b.x;
+        bf[s][1] = b.y;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int mi = 0; mi < C::WT_M; ++mi) {
+        const double a = s ? af[mi].y : af[mi].x;
+#pragma unroll
+        for (int p = 0; p < C::NPAR; ++p) dmma(acc.v[mi][p][0], acc.v[mi][p][1], a, bf[s][p]);
+      }
+  }
+}
+
+// tools/k6c_probe.cu defines K6C_PROF to timestamp the phases of a few stages (not in the library)
+#ifdef K6C_PROF
+__device__ long long g_k6c_prof[2][16][8];
+#define K6C_MARK(i)                                                                              \
+  if (blockIdx.x < 2 && threadIdx.x == 0 && t >= 200 && t < 216) g_k6c_prof[blockIdx.x][t - 200][i] = clock64();
+#else
+#define K6C_MARK(i)
+#endif
+
+template <int NP, int CS>
+__global__ void __launch_bounds__(ClusterCfg<NP, CS>::THREADS, 1)
+    fine_cluster_kernel(int flow, int n, int ld, const double* __restrict__ M, const double* __restrict__ Uin,
+                        double* __restrict__ Fout, long long mstride, int mF, double h, const int* stop_flag) {
+  using C = ClusterCfg<NP, CS>;
+  extern __shared__ double sm[];
+  __shared__ __align__(8) uint64_t xbar[2];
+  __shared__ int s_stop;
+  double* sM = sm;
+  double* sX = sM + C::MAT;
+  double* sYa = sX + C::MAT;
+  double* sYb = sYa + C::MAT;
+  double* sW = sYb + C::MAT;
+  const uint32_t q = cluster_ctarank();
+  const int z = blockIdx.x / CS;
+  if (threadIdx.x == 0) {
+    s_stop = (stop_flag != nullptr && *(volatile const int*)stop_flag != 0) ? 1 : 0;
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    fence_barrier_init();
+  }
+  cluster_sync_all();
+  // the cluster follows rank 0's reading of the (concurrently written) stop flag
+  const bool stop = ld_cluster_s32(mapa_u32(smem_u32(&s_stop), 0)) != 0;
+  if (!stop) {
+    load_mat<NP>(sM, M, n, ld);
+    load_mat<NP>(sX, Uin + z * mstride, n, ld);
+    for (int i = threadIdx.x; i < C::MAT; i += blockDim.x) sYa[i] = sYb[i] = sW[i] = 0.0;
+    __syncthreads();
+    const ClPos<NP, CS> o(q);
+    const bool xchg = (flow != 2);   // exp: K = A Y[:, own] is column-local
+    ClAFrag<NP, CS> mfr;             // the constant left operand (B or A) as register fragments
+    if (flow == 0 || flow == 2) {
+#pragma unroll
+      for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+        for (int kb = 0; kb < NP / 8; ++kb)
+          mfr.f[mi][kb] = *reinterpret_cast<const double2*>(sM + sidx<NP>(o.row(mi), 8 * kb + 2 * o.c));
+    }
+    ClAcc<NP, CS> xr, sr;
+#pragma unroll
+    for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+      for (int p = 0; p < C::NPAR; ++p)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          xr.v[mi][p][e] = sX[sidx<NP>(o.row(mi), o.col(p, e))];
+          sr.v[mi][p][e] = 0.0;
+        }
+    // peer CTAs' shared-memory windows (same dynamic-smem offsets in every CTA of the cluster)
+    uint32_t rsm[CS > 1 ? CS - 1 : 1], rbar[CS > 1 ? CS - 1 : 1];
+#pragma unroll
+    for (int r = 1; r < CS; ++r) {
+      rsm[r - 1] = mapa_u32(smem_u32(sm), (q + r) % CS);
+      rbar[r - 1] = mapa_u32(smem_u32(&xbar[0]), (q + r) % CS);
+    }
+    const double h6 = h / 6.0;
+    const int nT = 4 * mF;
+    for (int t = 0; t < nT; ++t) {
+      const int s = (t & 3) + 1;
+      const double* Yin = (s == 1) ? sX : (s == 3 ? sYb : sYa);
+      double* Yout = (s == 4) ? sX : ((s == 2) ? sYb : sYa);
+      const bool send = xchg && (t + 1 < nT);
+      K6C_MARK(0);
+      if (send && threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[t & 1], C::XBYTES);
+      ClAcc<NP, CS> K;
+      if (flow == 0) {   // W[:, own] = B Y[:, own] (local), then K = Y W[:, own] (needs all of Y)
+        ClAcc<NP, CS> w;
+        cl_gemm<NP, CS, true>(o, sM, Yin, w, &mfr);
+        K6C_MARK(1);
+#pragma unroll
+        for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if constexpr (C::NPAR == 2) {   // columns (par 0, par 1) are one 16-byte pair
+              *reinterpret_cast<double2*>(sW + sidx<NP>(o.row(mi), o.col(0, e))) =
+                  make_double2(w.v[mi][0][e], w.v[mi][1][e]);
+            } else {
+              sW[sidx<NP>(o.row(mi), o.col(0, e))] = w.v[mi][0][e];
+            }
+          }
+        __syncthreads();
+        K6C_MARK(2);
+        if (t > 0) mbar_wait(&xbar[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        K6C_MARK(3);
+        cl_gemm<NP, CS, false>(o, Yin, sW, K, nullptr);
+        K6C_MARK(4);
+      } else if (flow == 2) {   // exp: K = A Y[:, own]
+        cl_gemm<NP, CS, true>(o, sM, Yin, K, &mfr);
+      } else {                  // sqrt: K = -(Y Y[:, own]) + A[:, own]
+        if (t > 0) mbar_wait(&xbar[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        cl_gemm<NP, CS, false>(o, Yin, Yin, K, nullptr);
+#pragma unroll
+        for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+          for (int p = 0; p < C::NPAR; ++p)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              K.v[mi][p][e] = fma(-1.0, K.v[mi][p][e], 1.0 * sM[sidx<NP>(o.row(mi), o.col(p, e))]);
+      }
+      // RK stage combination on the owned elements (epilogue.cuh EPI_RK arithmetic), new Y to the
+      // local copy and to every peer
+      const double cy = (s == 3) ? h : 0.5 * h;
+      const uint32_t yoff = 8u * (uint32_t)(Yout - sm), boff = 8u * (uint32_t)(t & 1);
+#pragma unroll
+      for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double out[C::NPAR];
+#pragma unroll
+          for (int p = 0; p < C::NPAR; ++p) {
+            const double k = K.v[mi][p][e];
+            double& x = xr.v[mi][p][e];
+            double& sv = sr.v[mi][p][e];
+            if (s == 4) {
+              x = fma(h6, sv + k, x);
+              out[p] = x;
+            } else {
+              sv = (s == 1) ? k : fma(2.0, k, sv);
+              out[p] = fma(cy, k, x);
+            }
+          }
+          const uint32_t off = 8u * (uint32_t)sidx<NP>(o.row(mi), o.col(0, e));
+          if constexpr (C::NPAR == 2) {
+            *reinterpret_cast<double2*>(Yout + off / 8) = make_double2(out[0], out[1]);
+          } else {
+            Yout[off / 8] = out[0];
+          }
+          if (send) {
+#pragma unroll
+            for (int r = 0; r < CS - 1; ++r) {
+              if constexpr (C::NPAR == 2) {
+                st_async_v2(rsm[r] + yoff + off, out[0], out[1], rbar[r] + boff);
+              } else {
+                st_async_1(rsm[r] + yoff + off, out[0], rbar[r] + boff);
+              }
+            }
+          }
+        }
+      K6C_MARK(5);
+      __syncthreads();
+      K6C_MARK(6);
+    }
+    // result: the owned columns straight from the registers
+#pragma unroll
+    for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+      for (int p = 0; p < C::NPAR; ++p)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = o.row(mi), cc = o.col(p, e);
+          if (r < n && cc < n) Fout[z * mstride + (long long)r * ld + cc] = xr.v[mi][p][e];
+        }
+  }
+  cluster_sync_all();   // no CTA leaves while a peer may still touch its shared memory
+}
+
+// ------------------------------------------------------------------------------------------------
 // coarse sweep over local slices j = j0 .. nloc-1 (single CTA).
 //   V_{j0} = Vin;  for each j: g = G(V_j) (mG Euler steps);
 //   correct == 0 (Step 0): U[j+1] = g, Gold[j] = g

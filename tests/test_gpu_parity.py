@@ -424,6 +424,43 @@ def test_small_kernels_bitwise_equal_gemm_path(n, flow):
     assert res[0][0]["gpu_launches"] < res[1][0]["gpu_launches"]
 
 
+@pytest.mark.parametrize("n", [5, 17, 32, 33, 64])
+@pytest.mark.parametrize("flow", [0, 1, 2])
+def test_small_cluster_kernels_bitwise(n, flow):
+    """K6c (one slice over a cluster of 2/4/8 CTAs, column-split, Y exchanged through DSMEM each
+    stage) keeps each output element's DMMA sequence and epilogue arithmetic, so every cluster size
+    agrees bitwise with the one-CTA kernel and with the launch-per-GEMM path; the solve matches the
+    oracle.  Ragged n (5, 17, 33) leaves padded columns in some CTAs' column sets."""
+    if flow == 1:
+        A = workloads.random_spd(n, 5 + n).A + np.eye(n)
+        T, N, mG, mF = 20.0, 16, 2, 16
+    else:
+        A = workloads.random_spd(n, 10 + n).A
+        if flow == 2:
+            A = A - 1.5 * np.eye(n)
+        T, N, mG, mF = 1.0, 8, 1, 16
+    sizes = [1, 2, 4] + ([8] if n > 32 else [])
+    res = {}
+    for cs in sizes:
+        _, info, X = _solve_gpu(A, flow, T, N, mG, mF, 3, small_cluster=cs)
+        res[cs] = (info, X)
+    _, info0, X0 = _solve_gpu(A, flow, T, N, mG, mF, 3, small=0)
+    for cs in sizes:
+        assert np.array_equal(res[cs][1], X0), cs
+        assert res[cs][0]["deltas"] == info0["deltas"], cs
+    ref = dense.solve(A, flow, T, N, mG, mF, 3)
+    assert relF(X0, ref["X"]) <= 1e-12
+
+
+def test_small_cluster_option_validation():
+    A = workloads.random_spd(32, 1).A
+    s = mf.Solver(A, mf.FLOW_INVERSE, 1.0, 4, 1, 4)
+    with pytest.raises(mf.MfodeError):
+        s.set_option("small_cluster", 8)    # n <= 32 has 32 columns: at most 4 CTAs of 8
+    with pytest.raises(mf.MfodeError):
+        s.set_option("small_cluster", 3)
+
+
 @pytest.mark.parametrize("n", [40, 200])
 def test_exp_flow_vs_oracle(n):
     """§8(f) f1: exp flow (Example 2) on the same kernels: GPU vs oracle and vs expm."""
