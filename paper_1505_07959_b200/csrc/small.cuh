@@ -611,6 +611,26 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   __syncthreads();
   for (int j = j0; j < nloc; ++j) {
     double* X = sV;
+    // the correction's F(U^k_j) and G(U^k_j) terms do not depend on this slice's GEMMs: load them first
+    // so their global latency hides under the coarse step
+    SmallAcc<NP> fk, gold;
+    if (correct) {
+#pragma unroll
+      for (int mi = 0; mi < C::WT_M; ++mi)
+#pragma unroll
+        for (int gi = 0; gi < C::WT_G; ++gi)
+#pragma unroll
+          for (int par = 0; par < 2; ++par)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              int r, cc;
+              acc_pos<NP>(mi, gi, par, e, r, cc);
+              const bool in = r < n && cc < n;
+              const long long go = (long long)j * mstride + (long long)r * ld + cc;
+              fk.v[mi][gi][par][e] = in ? Fk[go] : 0.0;
+              gold.v[mi][gi][par][e] = in ? Gold[go] : 0.0;
+            }
+    }
     for (int i = 0; i < mG; ++i) {
       SmallAcc<NP> K;
       rhs_regs<NP>(flow, sM, X, sW, K);
@@ -636,7 +656,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
                 const long long go = (long long)j * mstride + (long long)r * ld + cc;
                 double u;
                 if (correct) {
-                  u = Fk[go] + (g - Gold[go]);
+                  u = fk.v[mi][gi][par][e] + (g - gold.v[mi][gi][par][e]);
                 } else {
                   u = g;
                 }
