@@ -444,7 +444,7 @@ def main():
             ms = float(np.mean([i["ms_total"] for i in ic]))
             sq = sc.sequential_fine()
             kf = ic[-1]
-            kname = ("K6 fine_smem_kernel" if wc.n <= 64 else
+            kname = ("K6c fine_cluster_kernel (one 2-CTA cluster per slice)" if wc.n <= 64 else
                      "K10 fine_fused_kernel" if wc.n <= 512 else "dgemm_tma_kernel (batched, fused RK epilogue)")
             secondary.append({
                 "workload": wc.name, "n": wc.n, "N_slices": wc.N, "k_done": kf["k_done"], "timed_solves": reps,
