@@ -221,6 +221,27 @@ def test_overlap_and_batch_invariance(overlap):
     assert np.array_equal(Xa, Xb)
 
 
+@pytest.mark.parametrize("cs", [1, 2, 4])
+def test_small_speculative_cancel_repeatable(cs):
+    """K6/K6c under speculation: the next sweep's fine launch is queued before the stop test and is
+    cancelled through the device stop flag when δ reaches tol; a cluster follows its rank-0 CTA's
+    reading of the flag, so a flag raised while the clusters start cannot split one (a split
+    cluster would hang on its exchange barrier).  Repeated solves must end, agree bitwise with the
+    strictly phased run, and stop at the same k."""
+    w = workloads.random_spd(32, 21)
+    _, i0, X0 = _solve_gpu(w.A, mf.FLOW_INVERSE, 1.0, 8, 1, 16, 8, 1e-9, mf.STOP_DELTA, overlap=0,
+                           small_cluster=cs)
+    assert 1 <= i0["k_done"] < 8
+    s = mf.Solver(w.A, mf.FLOW_INVERSE, 1.0, 8, 1, 16)
+    s.set_option("overlap", 1)
+    s.set_option("small_cluster", cs)
+    for _ in range(20):
+        info = s.solve(8, 1e-9, mf.STOP_DELTA)
+        assert info["k_done"] == i0["k_done"]
+        assert np.array_equal(s.result(), X0)
+    s.close()
+
+
 def test_identity_exact():
     """P7: A = I gives exactly I for both flows."""
     for flow in (mf.FLOW_INVERSE, mf.FLOW_SQRT):
