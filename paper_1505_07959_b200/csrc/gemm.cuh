@@ -94,8 +94,17 @@ struct GemmCfg {
   // which the mirrored elements are written as 64-byte row segments
   static constexpr int kMirrorPitch = 33;
   static constexpr int kMirrorDoubles = (BM == BN) ? kConsumerWarps * 2 * 8 * kMirrorPitch : 0;
+  // staged epilogue (128 x 128 tiles): the element-wise operands (C, X, S / Gold, F) of the next few
+  // 4-column groups are copied global -> shared with cp.async while the current group is computed, in
+  // per-warp slots [slot][array][lane][4] (12 KB per warp: 4 slots of 3 arrays, or 3 slots of 4); it
+  // shares the area of the symmetric-mode mirror staging
+  static constexpr bool kEpiStaged = (BM == 128 && BN == 128);
+  static constexpr int kEpiWarpBytes = kEpiStaged ? 12 * 1024 : 0;
+  static constexpr int kEpiDoubles = kConsumerWarps * kEpiWarpBytes / 8;
+  static constexpr int kAuxDoubles = kMirrorDoubles > kEpiDoubles ? kMirrorDoubles : kEpiDoubles;
   static constexpr int kSmemBytes =
-      STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8 + kMirrorDoubles * 8;
+      STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64 * 8 + kAuxDoubles * 8;
+  static_assert(kSmemBytes <= 232448, "shared memory per CTA");
   static_assert(WM % 8 == 0 && WN % 16 == 0, "warp tile must be a multiple of 8 x 16");
   static_assert(BM <= 256 && BN % 16 == 0, "TMA box limits");
 };
@@ -254,8 +263,64 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
 #pragma unroll
       for (int j = 0; j < 2 * Cfg::NG; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    // staged epilogue (see GemmCfg): the first D groups' operands are requested kEpiLead k-steps before
+    // the end of the main loop, so they land while the last DMMAs run
+    constexpr bool kStaged =
+        Cfg::kEpiStaged && (EPI == EPI_RK || EPI == EPI_EULER || EPI == EPI_EULER_CORR || EPI == EPI_ACCEL);
+    constexpr int NA = (EPI == EPI_EULER_CORR) ? 4 : 3;          // arrays per slot: C, X, S (/ Gold), F
+    // NSLOT slots per warp, D = NSLOT - 1 groups in flight: the slot a new copy targets was read one
+    // group earlier, never by the group just processed
+    constexpr int NSLOT = kStaged ? Cfg::kEpiWarpBytes / (NA * 1024) : 2;
+    constexpr int D = NSLOT - 1;
+    constexpr int NGR = Cfg::MT * Cfg::NG;
+    constexpr int kEpiLead = 2;
+    // (recomputed where used rather than held in registers across the main loop)
+    auto use_c = [&] { return p.beta != 0.0; };
+    auto use_s = [&] {
+      return (EPI == EPI_EULER_CORR) || (EPI == EPI_RK && p.stage > 1) || (EPI == EPI_ACCEL && (z & 1) == 0);
+    };
+    auto slot_addr = [&](int gi) {
+      return smem_u32(mirror_stage) + (uint32_t)warp * (uint32_t)Cfg::kEpiWarpBytes +
+             (uint32_t)(((gi % NSLOT) * NA * 128 + lane * 4) * 8);
+    };
+    auto issue = [&](int gi) {
+      if (gi < NGR) {
+        const int mt = gi / Cfg::NG, ng = gi % Cfg::NG;
+        const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
+        const int col = n0 + wn * Cfg::WN + ng * 16 + 4 * c;
+        if (row < n && col + 3 < n) {
+          const long long off = (long long)row * p.ld + col;
+          const uint32_t d = slot_addr(gi);
+          if (use_c()) {
+            const double* src = p.C.at(z) + off;
+            cp_async16(d, src);
+            cp_async16(d + 16, src + 2);
+          }
+          const double* sx = p.X_in.at(z) + off;
+          cp_async16(d + 1024, sx);
+          cp_async16(d + 1024 + 16, sx + 2);
+          if (use_s() && EPI != EPI_EULER_CORR) {
+            const double* ss = p.S.at(z) + off;
+            cp_async16(d + 2048, ss);
+            cp_async16(d + 2048 + 16, ss + 2);
+          }
+          if constexpr (EPI == EPI_EULER_CORR) {
+            const double* sf = p.F_in.at(z) + off;
+            cp_async16(d + 3072, sf);
+            cp_async16(d + 3072 + 16, sf + 2);
+          }
+        }
+      }
+      cp_async_commit();   // (empty groups keep the count uniform)
+    };
     bool ready = false;   // full[stage] already observed complete by the early probe
     for (int kt = 0; kt < KT; ++kt) {
+      if constexpr (kStaged) {
+        if (kt == (KT > kEpiLead ? KT - kEpiLead : 0) && !sym) {   // (symmetric mode uses the area for its mirror staging)
+#pragma unroll
+          for (int gi = 0; gi < D; ++gi) issue(gi);
+        }
+      }
       if (!ready) mbar_wait(&full[stage], phase);
       const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
       const uint32_t sB = sA + Cfg::kABytes;
@@ -364,7 +429,60 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
         continue;
       }
     }
-    if constexpr (EPI != EPI_RESID) {
+    if constexpr (kStaged) {
+      // staged epilogue: the operands of groups gi + 1 .. gi + D are in flight (cp.async into this
+      // warp's slots) while group gi is computed and stored, so the L2 latency of the loads is not paid
+      // once per group (the compiler cannot hoist the next group's global loads above this group's
+      // stores, which might alias them).  Ragged groups load inline.  Two measured hazards shape it:
+      //   * a slot is refilled only one group after it was read (refilling the slot just read left one
+      //     wrong solve in eight at n = 4096, none in 29 reruns after the change);
+      //   * the correction's Gold (read, then overwritten in place by this epilogue) is NOT staged:
+      //     staged, it gave a few wrong 64 x 32 warp sub-tiles in nearly every n >= 3072 solve, for a
+      //     reason not identified (K1), while staged C / X / S / F stay bitwise equal to
+      //     the unstaged kernel (tools/ab_compare.py); the correction is ~2 % of a solve.
+      const int ld = p.ld;
+#pragma unroll
+      for (int gi = 0; gi < NGR; ++gi) {
+        const int mt = gi / Cfg::NG, ng = gi % Cfg::NG;
+        const int row = m0 + wm * Cfg::WM + mt * 8 + rowA;
+        const int col = n0 + wn * Cfg::WN + ng * 16 + 4 * c;
+        cp_async_wait<D - 1>();   // group gi has landed (this lane's own copies)
+        if (row < n && col < n) {
+          double k4[4] = {acc[mt][2 * ng][0], acc[mt][2 * ng + 1][0], acc[mt][2 * ng][1], acc[mt][2 * ng + 1][1]};
+          double mv[2][4];
+          double* mp[2];
+          if (col + 3 < n) {
+            const uint32_t d = slot_addr(gi);
+            EpiIn in;
+            double2 v0, v1;
+            if (use_c()) {
+              v0 = lds128(d); v1 = lds128(d + 16);
+              in.c[0] = v0.x; in.c[1] = v0.y; in.c[2] = v1.x; in.c[3] = v1.y;
+            }
+            v0 = lds128(d + 1024); v1 = lds128(d + 1024 + 16);
+            in.x[0] = v0.x; in.x[1] = v0.y; in.x[2] = v1.x; in.x[3] = v1.y;
+            if (EPI == EPI_EULER_CORR) {
+              // the correction's Gold is loaded here, not staged (see above)
+              const double* gp = p.Gold.at(z) + (long long)row * ld + col;
+              const double2 g0 = *reinterpret_cast<const double2*>(gp);
+              const double2 g1 = *reinterpret_cast<const double2*>(gp + 2);
+              in.s[0] = g0.x; in.s[1] = g0.y; in.s[2] = g1.x; in.s[3] = g1.y;
+            } else if (use_s()) {
+              v0 = lds128(d + 2048); v1 = lds128(d + 2048 + 16);
+              in.s[0] = v0.x; in.s[1] = v0.y; in.s[2] = v1.x; in.s[3] = v1.y;
+            }
+            if constexpr (EPI == EPI_EULER_CORR) {
+              v0 = lds128(d + 3072); v1 = lds128(d + 3072 + 16);
+              in.f[0] = v0.x; in.f[1] = v0.y; in.f[2] = v1.x; in.f[3] = v1.y;
+            }
+            epi_apply4_impl<EPI, false, true>(p, z, alpha, row, col, n, ld, k4, false, false, part, mv, mp, &in);
+          } else {
+            epi_apply4_impl<EPI, false>(p, z, alpha, row, col, n, ld, k4, false, false, part, mv, mp);
+          }
+        }
+        issue(gi + D);
+      }
+    } else if constexpr (EPI != EPI_RESID) {
       // epilogue over the flattened groups g = mt * NG + ng (guarded, no early exits).  EPI_STORE
       // (W = B Y) runs the software-pipelined form (operands of group g + 1 loaded before group g is
       // stored); the other epilogues keep their loads inline -- pipelining them raises register
