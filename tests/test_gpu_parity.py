@@ -127,6 +127,38 @@ def test_rk_stage_parity(n, stage):
         assert np.all(np.abs(dYn.cpu().numpy() - refY) <= c * tolK + 4 * U53 * (np.abs(X) + c * np.abs(K)))
 
 
+@pytest.mark.parametrize("stage", [1, 2, 3, 4])
+@pytest.mark.parametrize("n", [300, 1030])
+def test_rk_stage_staged_epilogue_bitwise(n, stage):
+    """The 128 x 128 kernel stages the epilogue operands (C, X, S) through shared memory with
+    cp.async; the per-element arithmetic and k order are those of the 64 x 64 kernel, so both tile
+    configurations agree bitwise -- here at ragged n (partial tiles, partial 4-column groups) with the
+    beta C term of the sqrt flow."""
+    rng = np.random.default_rng(10 + stage)
+    Y, W, X, S, C = (rng.standard_normal((n, n)) for _ in range(5))
+    out = []
+    for tile in (1, 2):
+        dX, dS, dYn = _dev(X), _dev(S), _dev(np.zeros((n, n)))
+        mf.rk_stage(_dev(Y), _dev(W), dX, dS, dYn, stage, 1.0 / 64, C=_dev(C), alpha=-1.0, beta=1.0, tile=tile)
+        out.append((dX.cpu().numpy(), dS.cpu().numpy(), dYn.cpu().numpy()))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("flow,n", [(0, 300), (1, 300), (2, 300), (0, 515)])
+def test_staged_epilogue_solves_bitwise(flow, n):
+    """Whole solves through every staged epilogue (RK stages, Step 0 Euler, the correction with its
+    inline Gold) with 128 x 128 tiles agree bitwise with 64 x 64 tiles (no staging) at ragged n."""
+    A = workloads.random_spd(n, 40 + n).A
+    if flow == 1:
+        A = A + np.eye(n)
+    elif flow == 2:
+        A = A - 1.5 * np.eye(n)
+    res = [_solve_gpu(A, flow, 1.0, 4, 1, 3, 2, tile=t)[1:] for t in (1, 2)]
+    assert np.array_equal(res[0][1], res[1][1])
+    assert res[0][0]["deltas"] == res[1][0]["deltas"]
+
+
 def test_frobenius_parity():
     rng = np.random.default_rng(9)
     X, Y = rng.standard_normal((300, 300)), rng.standard_normal((300, 300))
