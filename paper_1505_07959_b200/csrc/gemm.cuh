@@ -263,8 +263,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
 #pragma unroll
       for (int j = 0; j < 2 * Cfg::NG; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // staged epilogue (see GemmCfg): the first D groups' operands are requested kEpiLead k-steps before
-    // the end of the main loop, so they land while the last DMMAs run
+    // staged epilogue (see GemmCfg): the first D groups' operands are requested when the main loop ends
     constexpr bool kStaged =
         Cfg::kEpiStaged && (EPI == EPI_RK || EPI == EPI_EULER || EPI == EPI_EULER_CORR || EPI == EPI_ACCEL);
     constexpr int NA = (EPI == EPI_EULER_CORR) ? 4 : 3;          // arrays per slot: C, X, S (/ Gold), F
@@ -273,7 +272,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     constexpr int NSLOT = kStaged ? Cfg::kEpiWarpBytes / (NA * 1024) : 2;
     constexpr int D = NSLOT - 1;
     constexpr int NGR = Cfg::MT * Cfg::NG;
-    constexpr int kEpiLead = 2;
     // (recomputed where used rather than held in registers across the main loop)
     auto use_c = [&] { return p.beta != 0.0; };
     auto use_s = [&] {
@@ -315,12 +313,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
     };
     bool ready = false;   // full[stage] already observed complete by the early probe
     for (int kt = 0; kt < KT; ++kt) {
-      if constexpr (kStaged) {
-        if (kt == (KT > kEpiLead ? KT - kEpiLead : 0) && !sym) {   // (symmetric mode uses the area for its mirror staging)
-#pragma unroll
-          for (int gi = 0; gi < D; ++gi) issue(gi);
-        }
-      }
       if (!ready) mbar_wait(&full[stage], phase);
       const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
       const uint32_t sB = sA + Cfg::kABytes;
@@ -433,14 +425,19 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, STAGES>::kTh
       // staged epilogue: the operands of groups gi + 1 .. gi + D are in flight (cp.async into this
       // warp's slots) while group gi is computed and stored, so the L2 latency of the loads is not paid
       // once per group (the compiler cannot hoist the next group's global loads above this group's
-      // stores, which might alias them).  Ragged groups load inline.  Two measured hazards shape it:
+      // stores, which might alias them).  Ragged groups load inline.  Measured hazards shaped it
+      // (profiles/staged_epilogue_r02.md):
       //   * a slot is refilled only one group after it was read (refilling the slot just read left one
       //     wrong solve in eight at n = 4096, none in 29 reruns after the change);
-      //   * the correction's Gold (read, then overwritten in place by this epilogue) is NOT staged:
-      //     staged, it gave a few wrong 64 x 32 warp sub-tiles in nearly every n >= 3072 solve, for a
-      //     reason not identified (K1), while staged C / X / S / F stay bitwise equal to
-      //     the unstaged kernel (tools/ab_compare.py); the correction is ~2 % of a solve.
+      //   * the first copies are issued when the main loop ends, not during its last k-steps: issued
+      //     2 k-steps early, the correction's Gold (read, then overwritten in place by this epilogue)
+      //     came back wrong in a few 64 x 32 warp sub-tiles of nearly every n >= 3072 solve, for a
+      //     reason not identified (issued after the loop: 6 of 6 right); the early issue was worth
+      //     only 0.15 %;
+      //   * belt and braces, the correction's Gold is not staged at all (~2 % of a solve).
       const int ld = p.ld;
+#pragma unroll
+      for (int gi = 0; gi < D; ++gi) issue(gi);
 #pragma unroll
       for (int gi = 0; gi < NGR; ++gi) {
         const int mt = gi / Cfg::NG, ng = gi % Cfg::NG;
