@@ -159,6 +159,19 @@ def test_staged_epilogue_solves_bitwise(flow, n):
     assert res[0][0]["deltas"] == res[1][0]["deltas"]
 
 
+@pytest.mark.parametrize("n,N,K", [(3072, 2, 1), (4096, 3, 2)])
+def test_staged_correction_large_n_bitwise(n, N, K):
+    """Regression guard for the staged epilogue at the sizes where its persistent CTAs run many tiles
+    (profiles/staged_epilogue_r02.md): whole sqrt-flow solves with 128 x 128 tiles (staged C / X / F,
+    inline Gold) equal the unstaged 64 x 64 kernel bitwise, twice over.  The dropped early-issue
+    variant (tools/experiments/gold_early_issue_r02.patch) fails exactly this comparison."""
+    A = workloads.random_spd(n, 7).A + np.eye(n)
+    ref = _solve_gpu(A, 1, 1.0, N, 1, 4, K, tile=1)[2]
+    for _ in range(2):
+        X = _solve_gpu(A, 1, 1.0, N, 1, 4, K, tile=2)[2]
+        assert np.array_equal(X, ref)
+
+
 def test_frobenius_parity():
     rng = np.random.default_rng(9)
     X, Y = rng.standard_normal((300, 300)), rng.standard_normal((300, 300))
