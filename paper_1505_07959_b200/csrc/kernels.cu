@@ -148,8 +148,12 @@ __global__ void k_copy_flag(const double* metric, double tol, int* stop_flag) {
 
 // ---- Frobenius subspace algebra of the modified parareal (§3) -------------------------
 // multi-dot: partials[i * gridDim.x + b] = sum over block b's fixed share of Q_i . V, i < count.
-// V is read once per block share, every Q_i once (HBM traffic (count + 1) * elems).
-constexpr int kMaxDots = 64;   // coefficients per multi-dot pass (the driver loops over passes)
+// V is read once per block share and pass, every Q_i once (HBM traffic (count + passes) * elems).
+// kMaxDots coefficients per pass keep the accumulators in registers at full occupancy (a 64-wide
+// pass needed 255 registers and spilled: one CTA per SM on a bandwidth-bound kernel).  Each
+// coefficient's summation order (thread share, warp shuffle, block sum) does not depend on the pass
+// width, so results are bitwise those of any other width.
+constexpr int kMaxDots = 16;   // coefficients per multi-dot pass (the driver loops over passes)
 
 __global__ void __launch_bounds__(kRedThreads) k_multidot(const double* Q, long long qstride, int count,
                                                           const double* V, long long total, double* partials) {
@@ -168,22 +172,21 @@ __global__ void __launch_bounds__(kRedThreads) k_multidot(const double* Q, long 
       }
     }
   }
-  __shared__ double red[kRedThreads / 32];
-  for (int i = 0; i < count; ++i) {
-    double a = acc[0];
-    // rotate so that acc[0] holds coefficient i (keeps acc[] in registers: constant indices only)
+  __shared__ double red[kMaxDots][kRedThreads / 32];
 #pragma unroll
-    for (int j = 0; j < kMaxDots - 1; ++j) acc[j] = acc[j + 1];
+  for (int i = 0; i < kMaxDots; ++i) {
+    if (i < count) {
+      double a = acc[i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < kRedThreads / 32; ++w) s += red[w];
-      partials[(long long)i * gridDim.x + blockIdx.x] = s;
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if ((threadIdx.x & 31) == 0) red[i][threadIdx.x >> 5] = a;
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x < count) {
+    double s = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) s += red[threadIdx.x][w];
+    partials[(long long)threadIdx.x * gridDim.x + blockIdx.x] = s;
   }
 }
 
