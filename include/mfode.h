@@ -102,7 +102,8 @@ typedef struct {
   double residual;     /* flow residual at U_N after the last sweep (see mfode_residual)         */
   double residual0;    /* flow residual after Step 0 (coarse sweep only)                         */
   double ms_total;     /* device time of the solve, max over ranks (CUDA events)                 */
-  double ms_fine;      /* device time of the last rank's fine stream busy period (informational) */
+  double ms_fine;      /* device time of the last rank's fine stream busy period (informational);
+                          modified parareal: sum of its fine-image spans (needs phase_timing) */
   double fine_flops;   /* algorithmic flops of the fine propagations performed (all ranks)       */
   double coarse_flops; /* algorithmic flops of coarse propagations + residual GEMMs (all ranks)  */
   int gpu_launches;    /* kernels launched by the solve (all logical ranks of this process)      */

@@ -93,7 +93,9 @@ struct NvtxRange {
 };
 
 // per-phase device timing (mfode_solve_info ms_coarse / ms_correct / ms_comm / ms_metric)
-enum Phase : int { PH_COARSE = 0, PH_CORRECT = 1, PH_COMM = 2, PH_METRIC = 3, PH_COUNT = 4 };
+enum Phase : int { PH_COARSE = 0, PH_CORRECT = 1, PH_COMM = 2, PH_METRIC = 3, PH_FINE = 4, PH_COUNT = 5 };
+// PH_FINE spans are recorded by the modified parareal only (its fine images are separate busy periods of
+// the fine stream; the classical solve times one ev_f0..ev_f1 period instead).
 
 // ---------------------------------------------------------------------------------------------
 // context
@@ -991,7 +993,7 @@ static int first_bad_slice(mfode_ctx* h) {
 
 // Sum the recorded phase spans of every local rank into info (events already complete).
 static int collect_phases(mfode_ctx* h, mfode_solve_info* info) {
-  double ph[PH_COUNT] = {0.0, 0.0, 0.0, 0.0};
+  double ph[PH_COUNT] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (auto& R : h->ranks)
     for (const auto& sp : R.spans) {
       float ms = 0.f;
@@ -1003,6 +1005,7 @@ static int collect_phases(mfode_ctx* h, mfode_solve_info* info) {
   info->ms_correct = ph[PH_CORRECT];
   info->ms_comm = ph[PH_COMM];
   info->ms_metric = ph[PH_METRIC];
+  if (ph[PH_FINE] > 0.0) info->ms_fine = ph[PH_FINE];
   return MFODE_OK;
 }
 
@@ -1407,6 +1410,8 @@ static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_
       NvtxRange nv("mfode:fine_images");
       CUDA_TRY(h, cudaEventRecord(R.ev_metric, st));
       CUDA_TRY(h, cudaStreamWaitEvent(R.fine, R.ev_metric, 0));
+      int fsp = -1;
+      TRY(span_open(h, R, R.fine, &fsp));
       for (int ja = nb_old; ja < nb; ja += h->cap) {
         const int jb = std::min(nb, ja + h->cap);
         TRY(fine_prop(h, R, h->Qb, h->bcap, h->FQ, h->bcap, ja, jb, nullptr));
@@ -1414,6 +1419,7 @@ static int modified_impl(mfode_ctx* h, int K_max, double tol, int stop, int max_
       // Algorithm 4: keep D_i = F(Q_i) - F(0) (Remark P:424-428)
       if (inhom) CUDA_TRY(h, launch_sub_bcast(slot(h, h->FQ, nb_old), tot, nb - nb_old, h->F0, tot, R.fine));
       fine_solves += nb - nb_old;
+      TRY(span_close(h, R, R.fine, PH_FINE, &fsp));
       CUDA_TRY(h, cudaEventRecord(R.ev_fine_end, R.fine));
       CUDA_TRY(h, cudaStreamWaitEvent(st, R.ev_fine_end, 0));
     }

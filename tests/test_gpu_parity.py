@@ -833,6 +833,23 @@ def test_phase_timings_reported():
     assert info0["ms_correct"] == 0.0 and info0["k_done"] == info["k_done"]
 
 
+def test_modified_parareal_phase_timings():
+    """The modified parareal (Algorithm 3) reports its fine images (ms_fine: the sum of
+    the fine-image spans) and its sequential projected update (ms_correct) as separate device
+    times inside ms_total; timing off changes nothing in the result."""
+    w = workloads.random_spd(256, 36, lo=0.5, hi=2.0)
+    s = mf.Solver(w.A, mf.FLOW_EXP, 1.0, 8, 1, 8)
+    s.solve_modified(1)
+    info = s.solve_modified(3)
+    X = s.result().copy()
+    assert info["ms_fine"] > 0.0 and info["ms_correct"] > 0.0
+    assert info["ms_fine"] + info["ms_correct"] <= info["ms_total"] * 1.001
+    s.set_option("phase_timing", 0)
+    info0 = s.solve_modified(3)
+    assert info0["ms_correct"] == 0.0 and info0["basis_size"] == info["basis_size"]
+    assert np.array_equal(s.result(), X)
+
+
 @pytest.mark.timeout(900)
 def test_cfg3_full_size_K1_vs_spectral_oracle():
     """BASELINE cfg[3] (the n = 4096 inverse flow of Example 1; BASELINE ties it to the
