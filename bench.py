@@ -420,7 +420,8 @@ def main():
     # mirrors them (half the executed flops).
     sym = variant({"symmetric": 1}, args.sym_steps) if args.sym_steps > 0 else None
     if sym and "time_to_tol_ms" in sym:
-        sym["executed_fine_tflops_approx"] = (sym["algorithmic_fine_tflops"] * (w.n // 128 + 1) / (2 * (w.n // 128)))
+        tiles = max(1, -(-w.n // 128))   # 128-wide tile rows (ceil): upper triangle incl. diagonal = t(t+1)/2 of t^2
+        sym["executed_fine_tflops_approx"] = sym["algorithmic_fine_tflops"] * (tiles + 1) / (2 * tiles)
     # f3(ii) every GEMM (except the residual's) emulated on the int8 tensor cores (CRT/Ozaki-II, exact
     # integer products of 55-bit-scaled operands), alone and combined with f3(i)
     emu = variant({"emulation": args.emu_moduli}, args.emu_steps) if args.emu_steps > 0 else None
